@@ -1,0 +1,309 @@
+// pq.cu — the standalone device LaB-PQ (Table tab:interface P:196-211),
+// array-based: a flag bitmap over the id universe plus a compacted
+// queue of the flagged ids.  Update sets the flag (test_and_set) and the
+// 0->1 winner appends; Extract(theta) reads the keys lazily and packs the
+// qualifying ids out, the rest into the other queue buffer.
+#include <stdio.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace sssp {
+
+struct __align__(128) PQCtrl {
+    int32_t size;      // |Q|
+    int32_t cnt_out;   // extract: qualifying ids
+    int32_t cnt_next;  // extract: remaining ids
+    int32_t err;       // latched range error
+    unsigned long long minv;
+    unsigned long long theta;
+};
+
+constexpr int kPQBlock = 256;
+constexpr int kSelBlock = 1024;
+
+__global__ void pq_update_kernel(const int32_t* __restrict__ ids, int64_t count, int32_t n, uint32_t* bm,
+                                 int32_t* queue, PQCtrl* c) {
+    const int lane = lane_id();
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = gw * 32; base < count; base += nwarps * 32) {
+        const int64_t i = base + lane;
+        bool app = false;
+        int32_t id = -1;
+        if (i < count) {
+            id = ids[i];
+            if (id < 0 || id >= n) {
+                atomicOr(&c->err, 1);
+            } else {
+                const uint32_t bit = 1u << (id & 31);
+                app = !(atomicOr(bm + (id >> 5), bit) & bit);  // test_and_set
+            }
+        }
+        const int32_t s = warp_append_slot(app, &c->size);
+        if (app) queue[s] = id;
+    }
+}
+
+__global__ void pq_count_kernel(const int32_t* __restrict__ queue, const uint64_t* __restrict__ keys, uint64_t theta,
+                                PQCtrl* c) {
+    const int32_t q = ld_volatile_i32(&c->size);
+    int32_t cnt = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += (int64_t)gridDim.x * blockDim.x)
+        cnt += ld_cg_u64(keys + queue[i]) <= theta;
+    cnt = warp_sum(cnt);
+    if (lane_id() == 0 && cnt) atomicAdd(&c->cnt_out, cnt);
+}
+
+__global__ void pq_extract_kernel(const int32_t* __restrict__ qcur, const uint64_t* __restrict__ keys, uint64_t theta,
+                                  int32_t* out, int32_t* qnext, uint32_t* bm, PQCtrl* c) {
+    const int32_t q = ld_volatile_i32(&c->size);
+    const int lane = lane_id();
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = gw * 32; base < q; base += nwarps * 32) {
+        const int64_t i = base + lane;
+        const bool valid = i < q;
+        const int32_t id = valid ? qcur[i] : 0;
+        const bool take = valid && ld_cg_u64(keys + id) <= theta;
+        const bool keep = valid && !take;
+        if (take) atomicAnd(bm + (id >> 5), ~(1u << (id & 31)));
+        const int32_t so = warp_append_slot(take, &c->cnt_out);
+        if (take) out[so] = id;
+        const int32_t sn = warp_append_slot(keep, &c->cnt_next);
+        if (keep) qnext[sn] = id;
+    }
+}
+
+__global__ void pq_finish_extract(PQCtrl* c) {
+    c->size = c->cnt_next;
+    c->cnt_next = 0;
+}
+
+__global__ void pq_min_kernel(const int32_t* __restrict__ queue, const uint64_t* __restrict__ keys, PQCtrl* c) {
+    const int32_t q = ld_volatile_i32(&c->size);
+    uint64_t mn = kInf;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = ld_cg_u64(keys + queue[i]);
+        mn = k < mn ? k : mn;
+    }
+    mn = warp_min_u64(mn);
+    if (lane_id() == 0 && mn != kInf) atomicMin(&c->minv, (unsigned long long)mn);
+}
+
+// ExtDist of rho-stepping over the queue, one CTA (reading R5/R6, round = 0).
+__global__ void __launch_bounds__(kSelBlock) pq_select_kernel(const int32_t* __restrict__ queue,
+                                                              const uint64_t* __restrict__ keys, uint64_t rho,
+                                                              uint64_t seed, uint32_t mode, uint64_t* samples,
+                                                              PQCtrl* c) {
+    __shared__ SelectSmem sm;
+    const int64_t q = ld_volatile_i32(&c->size);
+    uint64_t th;
+    if ((uint64_t)q <= rho) {
+        th = kInf;
+    } else if (mode == SSSP_SELECT_EXACT) {
+        th = cta_kth_smallest(QueueKey{queue, keys}, q, rho, sm);
+    } else {
+        const uint64_t s = sample_count((uint64_t)q, rho);
+        for (uint64_t j = threadIdx.x; j < s; j += blockDim.x) {
+            const uint64_t r = splitmix64(seed ^ splitmix64(j));  // round 0: (0 << 32) | j
+            samples[j] = ld_cg_u64(keys + queue[r % (uint64_t)q]);
+        }
+        __syncthreads();
+        uint64_t k = (rho * s + (uint64_t)q - 1) / (uint64_t)q;
+        k = k < 1 ? 1 : (k > s ? s : k);
+        th = cta_kth_smallest(ArrayKey{samples}, (int64_t)s, k, sm);
+    }
+    if (threadIdx.x == 0) c->theta = th;
+}
+
+}  // namespace sssp
+
+using namespace sssp;
+
+struct sssp_pq {
+    int32_t n;
+    const uint64_t* keys;
+    uint32_t* bm;
+    int32_t* q[2];
+    int cur;
+    uint64_t* samples;
+    PQCtrl* ctrl;
+    PQCtrl* h_ctrl;
+    cudaStream_t stream;
+    int device;
+    int grid;
+};
+
+namespace {
+struct PQLayout {
+    PQCtrl* ctrl;
+    uint32_t* bm;
+    int32_t *q0, *q1;
+    uint64_t* samples;
+    size_t bytes;
+};
+PQLayout pq_carve(void* base, int32_t n) {
+    Carver c(base);
+    PQLayout L;
+    L.ctrl = c.take<PQCtrl>(1);
+    L.bm = c.take<uint32_t>(((size_t)n + 31) / 32);
+    L.q0 = c.take<int32_t>(n);
+    L.q1 = c.take<int32_t>(n);
+    L.samples = c.take<uint64_t>(kMaxSamples);
+    L.bytes = align_up(c.off, 256);
+    return L;
+}
+
+// read back the control block; report a latched range error
+sssp_status pq_sync(sssp_pq* q, const char* what) {
+    cudaError_t e = cudaMemcpyAsync(q->h_ctrl, q->ctrl, sizeof(PQCtrl), cudaMemcpyDeviceToHost, q->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(q->stream);
+    if (e != cudaSuccess) return cuda_error(e, what);
+    if (q->h_ctrl->err) {
+        cudaMemsetAsync(&q->ctrl->err, 0, sizeof(int32_t), q->stream);
+        return set_error(SSSP_ERR_RANGE, "%s: an earlier sssp_pq_update got an id outside [0, %d)", what, q->n);
+    }
+    return SSSP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+size_t sssp_pq_workspace_bytes(int32_t n) {
+    if (n < 1 || n > 2147483646) return 0;
+    return pq_carve(nullptr, n).bytes;
+}
+
+sssp_status sssp_pq_create(int32_t n, const uint64_t* d_keys, void* d_ws, size_t ws_bytes, sssp_stream_t stream,
+                           sssp_pq** out) {
+    if (!out) return set_error(SSSP_ERR_INVALID, "sssp_pq_create: out is NULL");
+    *out = nullptr;
+    if (n < 1 || n > 2147483646) return set_error(SSSP_ERR_INVALID, "sssp_pq_create: n=%d outside [1, 2^31-2]", n);
+    if (!d_keys || !d_ws) return set_error(SSSP_ERR_INVALID, "sssp_pq_create: NULL pointer");
+    if ((uintptr_t)d_ws % 256) return set_error(SSSP_ERR_INVALID, "sssp_pq_create: workspace not 256-byte aligned");
+    if (ws_bytes < sssp_pq_workspace_bytes(n))
+        return set_error(SSSP_ERR_INVALID, "sssp_pq_create: workspace %zu < required %zu", ws_bytes,
+                         sssp_pq_workspace_bytes(n));
+    int dev = 0, sms = 0;
+    cudaError_t e = bind_device_of(d_ws, &dev);
+    if (e != cudaSuccess) return cuda_error(e, "sssp_pq_create: workspace is not device memory");
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    PQLayout L = pq_carve(d_ws, n);
+    sssp_pq* q = new sssp_pq();
+    q->n = n;
+    q->keys = d_keys;
+    q->bm = L.bm;
+    q->q[0] = L.q0;
+    q->q[1] = L.q1;
+    q->cur = 0;
+    q->samples = L.samples;
+    q->ctrl = L.ctrl;
+    q->stream = (cudaStream_t)stream;
+    q->grid = sms * 8;
+    q->device = dev;
+    e = cudaMallocHost((void**)&q->h_ctrl, sizeof(PQCtrl));
+    if (e == cudaSuccess) e = cudaMemsetAsync(L.ctrl, 0, sizeof(PQCtrl), q->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(L.bm, 0, ((size_t)n + 31) / 32 * sizeof(uint32_t), q->stream);
+    if (e != cudaSuccess) {
+        if (q->h_ctrl) cudaFreeHost(q->h_ctrl);
+        delete q;
+        return cuda_error(e, "sssp_pq_create");
+    }
+    *out = q;
+    return SSSP_OK;
+}
+
+sssp_status sssp_pq_update(sssp_pq* q, const int32_t* d_ids, int64_t count) {
+    if (!q) return set_error(SSSP_ERR_INVALID, "sssp_pq_update: NULL queue");
+    cudaSetDevice(q->device);
+    if (count < 0 || (count > 0 && !d_ids)) return set_error(SSSP_ERR_INVALID, "sssp_pq_update: bad batch");
+    if (count == 0) return SSSP_OK;
+    int64_t blocks = (count + kPQBlock - 1) / kPQBlock;
+    if (blocks > q->grid) blocks = q->grid;
+    pq_update_kernel<<<(unsigned)blocks, kPQBlock, 0, q->stream>>>(d_ids, count, q->n, q->bm, q->q[q->cur], q->ctrl);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SSSP_OK : cuda_error(e, "sssp_pq_update");
+}
+
+sssp_status sssp_pq_size(sssp_pq* q, int64_t* h_size) {
+    if (!q || !h_size) return set_error(SSSP_ERR_INVALID, "sssp_pq_size: NULL argument");
+    cudaSetDevice(q->device);
+    sssp_status s = pq_sync(q, "sssp_pq_size");
+    *h_size = q->h_ctrl->size;
+    return s;
+}
+
+sssp_status sssp_pq_extract(sssp_pq* q, uint64_t theta, int32_t* d_out, int64_t cap, int64_t* h_count) {
+    if (!q || !h_count) return set_error(SSSP_ERR_INVALID, "sssp_pq_extract: NULL argument");
+    cudaSetDevice(q->device);
+    if (cap < 0 || (cap > 0 && !d_out)) return set_error(SSSP_ERR_INVALID, "sssp_pq_extract: bad output buffer");
+    cudaError_t e = cudaMemsetAsync(&q->ctrl->cnt_out, 0, sizeof(int32_t), q->stream);
+    if (e != cudaSuccess) return cuda_error(e, "sssp_pq_extract");
+    pq_count_kernel<<<q->grid, kPQBlock, 0, q->stream>>>(q->q[q->cur], q->keys, theta, q->ctrl);
+    sssp_status s = pq_sync(q, "sssp_pq_extract");
+    if (s != SSSP_OK) return s;
+    *h_count = q->h_ctrl->cnt_out;
+    if (q->h_ctrl->cnt_out > cap)
+        return set_error(SSSP_ERR_CAPACITY, "sssp_pq_extract: %d ids qualify, cap %lld", q->h_ctrl->cnt_out,
+                         (long long)cap);
+    cudaMemsetAsync(&q->ctrl->cnt_out, 0, 2 * sizeof(int32_t), q->stream);  // cnt_out, cnt_next
+    pq_extract_kernel<<<q->grid, kPQBlock, 0, q->stream>>>(q->q[q->cur], q->keys, theta, d_out, q->q[q->cur ^ 1], q->bm,
+                                                           q->ctrl);
+    pq_finish_extract<<<1, 1, 0, q->stream>>>(q->ctrl);
+    q->cur ^= 1;
+    s = pq_sync(q, "sssp_pq_extract");
+    if (s == SSSP_OK) *h_count = q->h_ctrl->cnt_out;
+    return s;
+}
+
+sssp_status sssp_pq_select(sssp_pq* q, uint64_t rho, uint64_t seed, uint32_t mode, uint64_t* h_theta) {
+    if (!q || !h_theta) return set_error(SSSP_ERR_INVALID, "sssp_pq_select: NULL argument");
+    cudaSetDevice(q->device);
+    if (rho == 0) return set_error(SSSP_ERR_INVALID, "sssp_pq_select: rho must be >= 1");
+    if (mode != SSSP_SELECT_SAMPLED && mode != SSSP_SELECT_EXACT)
+        return set_error(SSSP_ERR_INVALID, "sssp_pq_select: unknown mode %u", mode);
+    pq_select_kernel<<<1, kSelBlock, 0, q->stream>>>(q->q[q->cur], q->keys, rho, seed, mode, q->samples, q->ctrl);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_error(e, "sssp_pq_select");
+    sssp_status s = pq_sync(q, "sssp_pq_select");
+    *h_theta = q->h_ctrl->theta;
+    return s;
+}
+
+sssp_status sssp_pq_reduce_min(sssp_pq* q, uint64_t* h_min) {
+    if (!q || !h_min) return set_error(SSSP_ERR_INVALID, "sssp_pq_reduce_min: NULL argument");
+    cudaSetDevice(q->device);
+    const unsigned long long inf = kInf;
+    cudaError_t e = cudaMemcpyAsync(&q->ctrl->minv, &inf, sizeof(inf), cudaMemcpyHostToDevice, q->stream);
+    if (e != cudaSuccess) return cuda_error(e, "sssp_pq_reduce_min");
+    pq_min_kernel<<<q->grid, kPQBlock, 0, q->stream>>>(q->q[q->cur], q->keys, q->ctrl);
+    sssp_status s = pq_sync(q, "sssp_pq_reduce_min");
+    *h_min = q->h_ctrl->minv;
+    return s;
+}
+
+sssp_status sssp_pq_queue(sssp_pq* q, int32_t* d_out, int64_t cap, int64_t* h_count) {
+    if (!q || !h_count) return set_error(SSSP_ERR_INVALID, "sssp_pq_queue: NULL argument");
+    cudaSetDevice(q->device);
+    sssp_status s = pq_sync(q, "sssp_pq_queue");
+    if (s != SSSP_OK) return s;
+    const int64_t sz = q->h_ctrl->size;
+    *h_count = sz;
+    if (sz > cap) return set_error(SSSP_ERR_CAPACITY, "sssp_pq_queue: |Q| = %lld > cap %lld", (long long)sz, (long long)cap);
+    if (sz == 0) return SSSP_OK;
+    if (!d_out) return set_error(SSSP_ERR_INVALID, "sssp_pq_queue: NULL d_out");
+    cudaError_t e = cudaMemcpyAsync(d_out, q->q[q->cur], (size_t)sz * sizeof(int32_t), cudaMemcpyDeviceToDevice, q->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(q->stream);
+    return e == cudaSuccess ? SSSP_OK : cuda_error(e, "sssp_pq_queue");
+}
+
+sssp_status sssp_pq_destroy(sssp_pq* q) {
+    if (!q) return SSSP_OK;
+    if (q->h_ctrl) cudaFreeHost(q->h_ctrl);
+    delete q;
+    return SSSP_OK;
+}
+
+}  // extern "C"

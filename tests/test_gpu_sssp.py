@@ -1,0 +1,228 @@
+"""GPU parity: sssp_run (the persistent round loop) vs the CPU oracle, through the C ABI.
+
+Distances must match the oracle's Dijkstra bit-exactly (integer arithmetic).  For the
+deterministic policies (Bellman-Ford, Delta*, exact rho, Dijkstra) the per-round trace
+(|Q_r|, |F_r|, E_r, inserts_r, theta_r) must equal the oracle's stepping simulation
+exactly (snapshot semantics, reading R8).
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from conftest import golden_value, load_golden, rng_graphs
+
+pytestmark = pytest.mark.gpu
+
+INF = oracle.INF_INT
+SPEC = load_golden("spec_examples.json")
+
+
+def _P():
+    import paper_2105_06145_b200 as P
+
+    return P
+
+
+def _run(h, g, pol, par, **kw):
+    P = _P()
+    return P.dist_to_u64(h.run(g.source, pol, par, **kw))
+
+
+def _assert_same(got, want, label):
+    if not np.array_equal(got, want):
+        bad = np.flatnonzero(got != want)
+        v = int(bad[0])
+        raise AssertionError(f"{label}: {len(bad)} mismatches; vertex {v} got {got[v]} want {want[v]}")
+
+
+SMALL_POLICIES = [("rho", 1), ("rho", 3), ("rho", 64), ("rho", 1 << 21), ("delta", 1), ("delta", 77),
+                  ("delta", 4096), ("delta", 1 << 30), ("bellman_ford", 0), ("dijkstra", 0)]
+
+
+def test_golden_examples(cuda_device):
+    P = _P()
+    for c in SPEC["sssp"]:
+        arcs = np.array(c["arcs"]).reshape(-1, 3)
+        g = gen.from_arcs(c["n"], arcs[:, 0], arcs[:, 1], arcs[:, 2], symmetrise=True, source=c["source"])
+        want = np.array(golden_value(c["dist"]), dtype=np.uint64)
+        h = P.SSSP.from_graph(g, validate=True)
+        for pol, par in SMALL_POLICIES:
+            _assert_same(_run(h, g, pol, par), want, f"{c['name']}/{pol}/{par}")
+        if "bf_rounds" in c:
+            _, st, tr, _ = h.run(g.source, "bellman_ford", 0, trace_cap=64)
+            assert st["rounds"] == c["bf_rounds"]
+            assert tr["fsize"].tolist() == c["bf_visited_per_round"]
+
+
+@pytest.mark.parametrize("name", ["grid64", "rmat12", "rgg64k", "rmat14log", "grid256"])
+def test_configs_small_all_policies(cuda_device, name):
+    P = _P()
+    g = gen.make(name)
+    want = oracle.dijkstra(g)
+    h = P.SSSP.from_graph(g, validate=True)
+    for pol, par in SMALL_POLICIES + [("rho", 1 << 10), ("rho", 1 << 15)]:
+        got = _run(h, g, pol, par)
+        _assert_same(got, want, f"{name}/{pol}/{par}")
+    for pol, par in (("rho", 256), ("rho", 4096)):
+        _assert_same(_run(h, g, pol, par, exact=True), want, f"{name}/{pol}/{par}/exact")
+        _assert_same(_run(h, g, pol, par, warmup=False), want, f"{name}/{pol}/{par}/nowarm")
+
+
+def test_random_graphs(cuda_device):
+    P = _P()
+    for g in rng_graphs(60, seed0=101, nmax=3000):
+        want = oracle.dijkstra(g)
+        h = P.SSSP.from_graph(g)
+        for pol, par in (("rho", 2), ("rho", 100), ("delta", 1000), ("bellman_ford", 0), ("dijkstra", 0)):
+            _assert_same(_run(h, g, pol, par), want, f"{g.name}/src{g.source}/{pol}/{par}")
+
+
+def test_edge_cases(cuda_device):
+    P = _P()
+    # n = 1, m = 0
+    g = gen.from_arcs(1, [], [], [])
+    h = P.SSSP.from_graph(g)
+    for pol, par in SMALL_POLICIES:
+        assert _run(h, g, pol, par).tolist() == [0]
+    # isolated source in a larger graph
+    g = gen.from_arcs(5, [1, 2], [2, 3], [4, 4], symmetrise=True, source=0)
+    h = P.SSSP.from_graph(g)
+    assert _run(h, g, "rho", 2).tolist() == [0, INF, INF, INF, INF]
+    # self-loops and parallel arcs in a user CSR are accepted (reading R11)
+    off = np.array([0, 3, 4, 4], np.int32)
+    idx = np.array([0, 1, 1, 2], np.int32)
+    w = np.array([5, 9, 2, 1], np.uint32)
+    g = gen.Graph(n=3, m=4, offsets=off, indices=idx, weights=w, source=0)
+    h = P.SSSP.from_graph(g, validate=True)
+    for pol, par in SMALL_POLICIES:
+        assert _run(h, g, pol, par).tolist() == [0, 2, 3]
+    # maximum weights: distances beyond 2^32
+    g = gen.chain(300, np.full(299, 0xFFFFFFFF, np.uint32))
+    h = P.SSSP.from_graph(g)
+    for pol, par in (("rho", 7), ("delta", 1 << 40), ("bellman_ford", 0)):
+        d = _run(h, g, pol, par)
+        assert int(d[-1]) == 299 * 0xFFFFFFFF
+    # a vertex of degree > 64 * 256 (heavy path, many chunks) plus light vertices
+    rs = np.random.default_rng(4)
+    n = 30000
+    src = np.concatenate([np.zeros(n - 1, np.int64), rs.integers(0, n, 40000)])
+    dst = np.concatenate([np.arange(1, n), rs.integers(0, n, 40000)])
+    wt = rs.integers(1, 1000, len(src)).astype(np.uint32)
+    g = gen.from_arcs(n, src, dst, wt, symmetrise=True, source=int(rs.integers(1, n)))
+    want = oracle.dijkstra(g)
+    h = P.SSSP.from_graph(g)
+    for pol, par in SMALL_POLICIES:
+        _assert_same(_run(h, g, pol, par), want, f"hub/{pol}/{par}")
+
+
+def test_errors(cuda_device):
+    P = _P()
+    g = gen.make("grid64")
+    h = P.SSSP.from_graph(g)
+    with pytest.raises(P.SSSPError) as e:
+        h.run(g.n, "rho", 4)
+    assert e.value.status == P.SSSP_ERR_RANGE
+    with pytest.raises(P.SSSPError) as e:
+        h.run(-1, "bellman_ford", 0)
+    assert e.value.status == P.SSSP_ERR_RANGE
+    for pol in ("rho", "delta"):
+        with pytest.raises(P.SSSPError) as e:
+            h.run(0, pol, 0)
+        assert e.value.status == P.SSSP_ERR_INVALID
+    with pytest.raises(P.SSSPError) as e:
+        h.run(0, "bellman_ford", 0, max_rounds=3)
+    assert e.value.status == P.SSSP_ERR_ROUNDS
+    # SSSP_VALIDATE rejects malformed graphs
+    import torch
+
+    for bad in ("weight0", "index", "offsets"):
+        off = torch.tensor(g.offsets, device="cuda")
+        idx = torch.tensor(g.indices, device="cuda")
+        w = torch.tensor(g.weights.view(np.int32), device="cuda")
+        if bad == "weight0":
+            w[5] = 0
+        elif bad == "index":
+            idx[7] = g.n
+        else:
+            off[10] = off[12] + 1
+        with pytest.raises(P.SSSPError) as e:
+            P.SSSP(off, idx, w, validate=True)
+        assert e.value.status == P.SSSP_ERR_INVALID_GRAPH
+
+
+TRACE_FIELDS = ["qsize", "fsize", "edges", "inserts", "theta"]
+
+
+@pytest.mark.parametrize("name", ["grid64", "rmat12", "rgg64k", "rmat14log"])
+def test_round_trace_parity(cuda_device, name):
+    """Per-round |Q|, |F|, E, inserts and theta equal the oracle's Alg. 1 simulation."""
+    P = _P()
+    g = gen.make(name)
+    d_ref, hops = oracle.dijkstra(g, with_hops=True)
+    kn = int(hops.max())
+    h = P.SSSP.from_graph(g)
+    cases = [("bellman_ford", 0, {}), ("delta", 1000, {}), ("delta", 20000, {}), ("dijkstra", 0, {}),
+             ("rho", 64, dict(exact=True, warmup=False)), ("rho", 2048, dict(exact=True, warmup=False)),
+             ("rho", 512, dict(exact=True, warmup=True))]
+    for pol, par, kw in cases:
+        d, st, tr, ext = h.run(g.source, pol, par, trace_cap=1 << 16, ext_counts=True, **kw)
+        d = P.dist_to_u64(d)
+        _assert_same(d, d_ref, f"{name}/{pol}/{par}")
+        _, tr_ref, ext_ref = oracle.stepping_sim(g, pol, par, exact=kw.get("exact", True),
+                                                 warmup=kw.get("warmup", False), ext_counts=True)
+        assert st["rounds"] == len(tr_ref), (pol, par, st["rounds"], len(tr_ref))
+        for f in TRACE_FIELDS:
+            if not np.array_equal(tr[f], tr_ref[f]):
+                r = int(np.flatnonzero(tr[f] != tr_ref[f])[0])
+                raise AssertionError(f"{name}/{pol}/{par} round {r + 1} {f}: gpu {tr[f][r]} oracle {tr_ref[f][r]}")
+        _assert_same(ext.cpu().numpy(), ext_ref, f"{name}/{pol}/{par} extraction counts")
+        assert st["extracted"] == tr_ref["fsize"].sum() and st["edges"] == tr_ref["edges"].sum()
+        if pol == "bellman_ford":
+            assert st["rounds"] == kn + 1
+
+
+def test_sampled_rho_invariants(cuda_device):
+    """Sampled theta depends on queue order, so only invariants are compared."""
+    P = _P()
+    g = gen.make("rmat12")
+    d_ref, hops = oracle.dijkstra(g, with_hops=True)
+    kn = int(hops.max())
+    h = P.SSSP.from_graph(g)
+    for rho in (16, 256, 4096):
+        for seed in range(3):
+            d, st, tr, ext = h.run(g.source, "rho", rho, seed=seed, trace_cap=4096, ext_counts=True)
+            _assert_same(P.dist_to_u64(d), d_ref, f"rho{rho}/seed{seed}")
+            assert st["rounds"] >= kn + 1
+            reach = hops >= 0
+            e = ext.cpu().numpy()
+            assert (e[reach] <= np.maximum(hops[reach], 1)).all()  # Lemma num-ext
+            q = tr["qsize"]
+            assert (q[1:] == q[:-1] - tr["fsize"][:-1] + tr["inserts"][:-1]).all()
+            # |Q| <= rho rounds drain the queue (theta = INF)
+            small = q <= rho
+            assert (tr["theta"][small] == INF).all() and (tr["fsize"][small] == q[small]).all()
+
+
+def test_determinism_and_run_host(cuda_device):
+    import torch
+
+    P = _P()
+    g = gen.make("rmat14log")
+    want = oracle.dijkstra(g)
+    h = P.SSSP.from_graph(g)
+    outs = [_run(h, g, "rho", 512, seed=s) for s in range(10)]
+    for o in outs:
+        _assert_same(o, want, "repeat")
+    host = torch.empty(g.n, dtype=torch.int64, pin_memory=True)
+    h.run_host(g.source, "rho", 512, host)
+    _assert_same(host.numpy().view(np.uint64), want, "run_host")
+    # a handle on a non-default stream
+    s = torch.cuda.Stream()
+    off = torch.from_numpy(g.offsets).cuda()
+    idx = torch.from_numpy(g.indices).cuda()
+    w = torch.from_numpy(g.weights.view(np.int32)).cuda()
+    h2 = P.SSSP(off, idx, w, stream=s)
+    d = h2.run(g.source, "delta", 1 << 14)
+    s.synchronize()
+    _assert_same(P.dist_to_u64(d), want, "side stream")
