@@ -1,0 +1,313 @@
+#!/usr/bin/env python
+"""Benchmark: SSSP GTEPS of the stepping-algorithm hot path on B200 (BASELINE.json metric).
+
+A step = one sssp_run (Alg. 1, all rounds) from the workload's source on a resident
+graph; GTEPS = m / device time per source.  Default workload (N=1): R-MAT scale 24
+(BASELINE.json configs[3], the config the north-star target is quoted on), rho-stepping.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config rmat24] [--policy rho] [--param P]
+  python bench.py --impl reference ...   # the CPU oracle arm (bounded Dijkstra samples, rank 0 only)
+
+Multi-GPU (torchrun): the path has no exchange step; every rank runs an independent
+replica (its own source on a full copy of the graph) -> "scaling": "weak", no collective
+in the timed region other than the barriers and the max-over-ranks reduction.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_PARAM = {"rho": 1 << 18, "delta": 1 << 15, "bellman_ford": 0, "dijkstra": 0}
+CONFIG_DESC = {
+    "grid256": "2D 4-neighbour grid 256x256, weights U[1,65535], source 0",
+    "rmat20": "R-MAT scale 20, ef 16 (.57,.19,.19,.05), symmetrised+dedup, weights U[1,2^18), source = max degree",
+    "rgg4m": "random geometric 4-NN graph, 2^22 points, weight round(len*1e6)+1, source nearest (0.5,0.5)",
+    "rmat24": "R-MAT scale 24, ef 16 (.57,.19,.19,.05), symmetrised+dedup, weights log-uniform [1,2^20), "
+              "source = max degree",
+    "grid4096": "2D 4-neighbour grid 4096x4096, weights U[1,65535], source 0 (corner)",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="rmat24")
+    ap.add_argument("--policy", default="rho", choices=["rho", "delta", "bellman_ford", "dijkstra"])
+    ap.add_argument("--param", type=int, default=None)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-arc-budget", type=int, default=200_000_000)
+    ap.add_argument("--no-flush", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def load_traffic(config, policy):
+    """dram bytes per launch of the round-loop kernel from a committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d.get(f"{config}/{policy}")
+        return (int(e["dram_bytes_per_launch"]), e.get("source")) if e else (None, None)
+    except Exception:
+        return None, None
+
+
+def make_graph(name):
+    import gen
+
+    if name not in gen.CONFIGS:
+        raise SystemExit(f"unknown config {name}; choose from {sorted(gen.CONFIGS)}")
+    return gen.make(name)
+
+
+def emit(obj):
+    print(json.dumps(obj), flush=True)
+
+
+# ----------------------------------------------------------------------------- CPU oracle arms
+def cpu_oracle_sample(g, source, arc_budget):
+    """Bounded sample of the oracle (plain binary-heap Dijkstra, 1 thread) on the same graph."""
+    import oracle
+
+    t0 = time.perf_counter()
+    scanned, settled = oracle.dijkstra_budget(g, source, arc_budget)
+    dt = time.perf_counter() - t0
+    return scanned, settled, dt
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return  # rank 0 alone runs the CPU oracle arm
+    g = make_graph(args.config)
+    budget = min(g.m, 20_000_000)
+    for _ in range(args.warmup):
+        cpu_oracle_sample(g, g.source, budget)
+    tot_arcs, tot_t, settled = 0, 0.0, 0
+    for _ in range(args.steps):
+        a, s, dt = cpu_oracle_sample(g, g.source, budget)
+        tot_arcs += a
+        tot_t += dt
+        settled = s
+    gteps = tot_arcs / tot_t / 1e9
+    sample = (f"binary-heap Dijkstra (oracle/, 1 thread) from the workload source, stopped after {budget} arc "
+              f"scans ({settled} vertices settled) per step")
+    emit({"impl": "reference", "metric": "SSSP GTEPS (m / device time per source)", "value": gteps,
+          "unit": "GTEPS", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+          "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+          "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+          "config": {"workload": f"{args.config}: {CONFIG_DESC.get(args.config, args.config)}",
+                     "n": g.n, "m": g.m, "source": g.source},
+          "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": 1, "kind": "oracle", "sample": sample},
+          "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2105_06145_b200 as P
+
+    ws, rank, local = dist_env()
+    if ws != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {ws}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    param = DEFAULT_PARAM[args.policy] if args.param is None else args.param
+
+    t_gen = time.perf_counter()
+    g = make_graph(args.config)
+    t_gen = time.perf_counter() - t_gen
+    # replicas: rank 0 uses the workload source; other ranks a seeded random non-isolated vertex
+    source = g.source
+    if rank > 0:
+        rs = np.random.default_rng(1000 + rank)
+        deg = g.degrees
+        while True:
+            v = int(rs.integers(0, g.n))
+            if deg[v] > 0:
+                source = v
+                break
+    h = P.SSSP.from_graph(g, device=dev)
+    stream = h.stream
+    out = torch.empty(g.n, dtype=torch.int64, device=dev)
+    flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        h.run(source, args.policy, param, out=out, seed=args.seed)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    barrier()
+    step_ms, kern_ms, rounds = [], [], []
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    for k in range(args.steps):
+        if flush is not None:
+            flush.zero_()  # evict L2 (126 MB) between timed steps; not inside the events
+        ev0.record(stream)
+        h.run(source, args.policy, param, out=out, seed=args.seed + k)
+        ev1.record(stream)
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+        kern_ms.append(h.last_stats["kernel_ms"])
+        rounds.append(h.last_stats["rounds"])
+    barrier()
+    total_ms = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    clocks = sampler.stop()
+    ms_per_step = total_ms / args.steps
+    value = ws * g.m / (ms_per_step * 1e-3) / 1e9
+
+    # end-to-end: the public host-buffer call (distances land in pinned host memory)
+    host = torch.empty(g.n, dtype=torch.int64, pin_memory=True)
+    h.run_host(source, args.policy, param, host)
+    barrier()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        h.run_host(source, args.policy, param, host)
+    e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = ws * g.m * args.steps / e2e_s / 1e9
+
+    # algorithmic bytes from a counters run of the same workload
+    _, st, _, _ = h.run(source, args.policy, param, out=out, stats=True, seed=args.seed)
+    b_extract = 8 * st["queue_scanned"]
+    b_relax = 8 * st["extracted"] + 16 * st["edges"]
+    b_touched = b_extract + b_relax
+    kern_avg = statistics.mean(kern_ms)
+    peak, peak_src = load_peaks()
+    achieved = b_touched / (kern_avg * 1e-3) / 1e9
+    traffic, traffic_src = load_traffic(args.config, args.policy)
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        budget = min(g.m, args.cpu_arc_budget)
+        scanned, settled, dt = cpu_oracle_sample(g, source, budget)
+        cpu = {"value": scanned / dt / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+               "sample": f"binary-heap Dijkstra (oracle/, 1 host thread of {os.cpu_count()}) from the same source, "
+                         f"stopped after {scanned} arc scans ({settled} vertices settled), {dt:.1f} s"}
+    emit({"metric": "SSSP GTEPS (m / device time per source)", "value": value, "unit": "GTEPS", "n_gpus": ws,
+          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+          "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+          "config": {"workload": f"{args.config}: {CONFIG_DESC.get(args.config, args.config)}",
+                     "n": g.n, "m": g.m, "source": source, "policy": args.policy, "param": param,
+                     "parallelism": f"replicas x{ws} (independent sources, no collective)",
+                     "l2": "flushed between timed steps (256 MiB write)" if flush is not None else "not flushed",
+                     "rounds_median": statistics.median(rounds), "kernel_ms_mean": kern_avg,
+                     "grid": [st["grid_blocks"], st["block_threads"]], "gen_s": round(t_gen, 1)},
+          "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                       "traffic": traffic, "peak_source": peak_src,
+                       "frac_of_8TBps": achieved / 8000.0,
+                       "algorithmic_bytes_per_launch": b_touched,
+                       "bytes_formula": "8*sum|Q_r| + 8*sum|F_r| + 16*sum E_r (SURVEY 8(d) B_touched)",
+                       "traffic_source": traffic_src},
+          "cpu_baseline": cpu,
+          "e2e": {"value": e2e, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * g.n,
+                  "note": "sssp_run_host: graph resident (created once), source passed by value, "
+                          "n uint64 distances copied to pinned host memory each step"},
+          "gpu_launches": args.steps,
+          "clocks": clocks,
+          "counters": {k: st[k] for k in ("rounds", "extracted", "edges", "succ", "inserts", "queue_scanned",
+                                          "max_queue", "max_frontier")}})
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

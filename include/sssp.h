@@ -127,6 +127,7 @@ typedef struct {
     int64_t max_frontier;   /* max |F_r|          (STATS only)                  */
     int32_t grid_blocks;    /* persistent-kernel CTAs                           */
     int32_t block_threads;  /* threads per CTA                                  */
+    double kernel_ms;       /* device time of the round-loop launch (CUDA events on the handle's stream) */
 } sssp_run_stats;
 
 /* Single-source shortest paths from `source` with the given policy (Alg. 1).

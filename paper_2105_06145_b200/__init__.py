@@ -52,10 +52,10 @@ class sssp_run_stats(ctypes.Structure):
     _fields_ = [("rounds", ctypes.c_int64), ("extracted", ctypes.c_int64), ("edges", ctypes.c_int64),
                 ("succ", ctypes.c_int64), ("inserts", ctypes.c_int64), ("queue_scanned", ctypes.c_int64),
                 ("max_queue", ctypes.c_int64), ("max_frontier", ctypes.c_int64), ("grid_blocks", ctypes.c_int32),
-                ("block_threads", ctypes.c_int32)]
+                ("block_threads", ctypes.c_int32), ("kernel_ms", ctypes.c_double)]
 
     def as_dict(self):
-        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+        return {k: (float if k == "kernel_ms" else int)(getattr(self, k)) for k, _ in self._fields_}
 
 
 ROUND_FIELDS = ["qsize", "fsize", "edges", "inserts", "succ", "theta", "nheavy", "reserved"]
@@ -177,6 +177,7 @@ class SSSP:
         with torch.cuda.stream(self.stream):
             _check(sssp_run_ex(self._h, int(source), pol, int(param), ctypes.byref(o), _ptr(out), ctypes.byref(st)),
                    "sssp_run")
+        self.last_stats = st.as_dict()
         if not (stats or trace_cap or ext_counts):
             return out
         tr = None
@@ -199,6 +200,7 @@ class SSSP:
         st = sssp_run_stats()
         _check(sssp_run_host(self._h, int(source), pol, int(param), ctypes.c_void_p(out_host.data_ptr()),
                              ctypes.byref(st)), "sssp_run_host")
+        self.last_stats = st.as_dict()
         return out_host
 
     def close(self):

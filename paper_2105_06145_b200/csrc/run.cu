@@ -485,6 +485,7 @@ struct sssp_handle {
     Ctrl* ctrl;
     Ctrl* h_ctrl;  // pinned host mirror for result readback
     int device;
+    cudaEvent_t ev[2];
     int num_sms;
     int grid[4][2];
 };
@@ -611,9 +612,11 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
             h->grid[pol][st] = per_sm * sms;
         }
     e = cudaMallocHost((void**)&h->h_ctrl, sizeof(Ctrl));
+    if (e == cudaSuccess) e = cudaEventCreate(&h->ev[0]);
+    if (e == cudaSuccess) e = cudaEventCreate(&h->ev[1]);
     if (e != cudaSuccess) {
         delete h;
-        return cuda_error(e, "cudaMallocHost");
+        return cuda_error(e, "sssp_create: host resources");
     }
     // the barrier counter must start at a multiple of 2^31; the rest is reset per run
     e = cudaMemsetAsync(L.ctrl, 0, sizeof(Ctrl), h->stream);
@@ -668,8 +671,10 @@ sssp_status sssp_run_ex(sssp_handle* h, int32_t source, sssp_policy policy, uint
     KernelFn k = kernel_for(policy, st);
     const int grid = h->grid[policy][st];
     void* args[] = {&p};
+    cudaEventRecord(h->ev[0], h->stream);
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kBlock), args, 0, h->stream);
     if (e != cudaSuccess) return cuda_error(e, "round-loop launch");
+    cudaEventRecord(h->ev[1], h->stream);
     e = cudaMemcpyAsync(&h->h_ctrl->status, &h->ctrl->status, sizeof(Ctrl) - offsetof(Ctrl, status),
                         cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
@@ -687,6 +692,9 @@ sssp_status sssp_run_ex(sssp_handle* h, int32_t source, sssp_policy policy, uint
         stats->max_frontier = c->max_f;
         stats->grid_blocks = grid;
         stats->block_threads = kBlock;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]);
+        stats->kernel_ms = ms;
     }
     if (c->status == SSSP_ERR_ROUNDS)
         return set_error(SSSP_ERR_ROUNDS, "sssp_run: exceeded max_rounds=%lld", (long long)p.max_rounds);
@@ -714,6 +722,8 @@ sssp_status sssp_run_host(sssp_handle* h, int32_t source, sssp_policy policy, ui
 sssp_status sssp_destroy(sssp_handle* h) {
     if (!h) return SSSP_OK;
     if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
+    if (h->ev[0]) cudaEventDestroy(h->ev[0]);
+    if (h->ev[1]) cudaEventDestroy(h->ev[1]);
     delete h;
     return SSSP_OK;
 }

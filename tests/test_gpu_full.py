@@ -1,0 +1,42 @@
+"""Full-size parity on the five BASELINE.json configurations, in the launch configuration bench.py times.
+
+Every vertex's distance is compared with the oracle's Dijkstra (feasible at these sizes:
+~20 s for R-MAT 24 on one host core), and the optimality certificate is checked on the
+GPU output as an independent full-size property.
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+# (policy, param) per config: the bench defaults plus parameters that exercise other paths
+CASES = {
+    "grid256": [("rho", 1 << 12), ("rho", 1 << 21), ("delta", 1 << 13), ("bellman_ford", 0)],
+    "rmat20": [("rho", 1 << 15), ("rho", 1 << 18), ("delta", 1 << 13), ("bellman_ford", 0)],
+    "rgg4m": [("rho", 1 << 12), ("rho", 1 << 15), ("delta", 1 << 8), ("bellman_ford", 0)],
+    "rmat24": [("rho", 1 << 15), ("rho", 1 << 18), ("rho", 1 << 21), ("delta", 1 << 15), ("bellman_ford", 0)],
+    "grid4096": [("rho", 1 << 12), ("delta", 1 << 13), ("bellman_ford", 0)],
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_full_config(cuda_device, name):
+    import paper_2105_06145_b200 as P
+
+    g = gen.make(name)
+    want, hops = oracle.dijkstra(g, with_hops=True)
+    kn = int(hops.max())
+    h = P.SSSP.from_graph(g, validate=True)
+    for pol, par in CASES[name]:
+        got = P.dist_to_u64(h.run(g.source, pol, par))
+        if not np.array_equal(got, want):
+            bad = np.flatnonzero(got != want)
+            raise AssertionError(f"{name}/{pol}/{par}: {len(bad)} mismatches, first {bad[0]}: "
+                                 f"{got[bad[0]]} vs {want[bad[0]]}")
+        assert h.last_stats["rounds"] >= kn + 1  # snapshot semantics lower bound
+        if pol == "bellman_ford":
+            assert h.last_stats["rounds"] == kn + 1
+    assert oracle.certify(g, got) == 0
