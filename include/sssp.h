@@ -93,6 +93,10 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t *d_offsets, const in
 #define SSSP_RUN_RHO_EXACT 1u /* rho: exact rho-th smallest instead of sampling (test mode) */
 #define SSSP_RUN_NO_WARMUP 2u /* rho: disable "10% of rho at the first two dense rounds" */
 #define SSSP_RUN_STATS 4u     /* collect per-run counters (slower variant of the round loop)          */
+#define SSSP_RUN_SNAPSHOT 8u  /* deterministic rounds: Extract completes before any relax of the round
+                                 and every frontier vertex relaxes with its key at Extract (reading R8).
+                                 Default ("live"): light vertices relax while Extract is still running,
+                                 fewer barriers; distances are identical, round counts may differ.     */
 
 typedef struct {
     uint32_t flags;
@@ -113,7 +117,11 @@ typedef struct {
     int64_t succ;    /* successful WriteMins (schedule dependent)               */
     uint64_t theta;  /* ExtDist value                                          */
     int64_t nheavy;  /* extracted vertices relaxed through the heavy-chunk path */
-    int64_t reserved;
+    int64_t t_theta_ns;   /* device time of ExtDist (globaltimer, CTA 0 view)          */
+    int64_t t_extract_ns; /* device time of Extract (+ fused light relax)             */
+    int64_t t_relax_ns;   /* device time of the remaining relax phase                 */
+    int64_t reserved0;
+    int64_t reserved1;
 } sssp_round;
 
 typedef struct {

@@ -15,7 +15,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsssp.so")
+# SSSP_LIB selects an in-tree tuning variant built by build.py --out (same ABI)
+LIB_PATH = os.environ.get("SSSP_LIB") or os.path.join(_HERE, "libsssp.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -30,7 +31,7 @@ SSSP_RHO, SSSP_DELTA, SSSP_BELLMAN_FORD, SSSP_DIJKSTRA = 0, 1, 2, 3
 POLICIES = {"rho": SSSP_RHO, "delta": SSSP_DELTA, "bellman_ford": SSSP_BELLMAN_FORD, "bf": SSSP_BELLMAN_FORD,
             "dijkstra": SSSP_DIJKSTRA}
 SSSP_VALIDATE = 1
-SSSP_RUN_RHO_EXACT, SSSP_RUN_NO_WARMUP, SSSP_RUN_STATS = 1, 2, 4
+SSSP_RUN_RHO_EXACT, SSSP_RUN_NO_WARMUP, SSSP_RUN_STATS, SSSP_RUN_SNAPSHOT = 1, 2, 4, 8
 SSSP_SELECT_SAMPLED, SSSP_SELECT_EXACT = 0, 1
 
 
@@ -58,7 +59,9 @@ class sssp_run_stats(ctypes.Structure):
         return {k: (float if k == "kernel_ms" else int)(getattr(self, k)) for k, _ in self._fields_}
 
 
-ROUND_FIELDS = ["qsize", "fsize", "edges", "inserts", "succ", "theta", "nheavy", "reserved"]
+ROUND_FIELDS = ["qsize", "fsize", "edges", "inserts", "succ", "theta", "nheavy", "t_theta_ns", "t_extract_ns",
+                "t_relax_ns", "reserved0", "reserved1"]
+ROUND_WORDS = len(ROUND_FIELDS)
 
 _vp, _i32, _i64, _u64, _u32, _sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
                                     ctypes.c_uint32, ctypes.c_size_t)
@@ -151,7 +154,7 @@ class SSSP:
         return SSSP(off, idx, w, validate=validate)
 
     def run(self, source, policy="rho", param=0, out=None, stats=False, trace_cap=0, ext_counts=False,
-            exact=False, warmup=True, seed=0, max_rounds=0):
+            exact=False, warmup=True, seed=0, max_rounds=0, snapshot=False):
         """Alg. 1 from `source`; returns a uint64-valued int64 tensor of distances (INF = -1 as int64).
 
         With stats=True returns (dist, stats_dict, trace ndarray | None, ext_count tensor | None)."""
@@ -161,12 +164,12 @@ class SSSP:
             out = torch.empty(self.n, dtype=torch.int64, device=self.offsets.device)
         o = sssp_run_opts()
         o.flags = (SSSP_RUN_RHO_EXACT if exact else 0) | (0 if warmup else SSSP_RUN_NO_WARMUP) | \
-                  (SSSP_RUN_STATS if (stats or trace_cap) else 0)
+                  (SSSP_RUN_STATS if (stats or trace_cap) else 0) | (SSSP_RUN_SNAPSHOT if snapshot else 0)
         o.seed = seed
         o.max_rounds = max_rounds
         trace = None
         if trace_cap:
-            trace = torch.zeros(trace_cap * 8, dtype=torch.int64, device=out.device)
+            trace = torch.zeros(trace_cap * ROUND_WORDS, dtype=torch.int64, device=out.device)
             o.d_trace = trace.data_ptr()
             o.trace_cap = trace_cap
         ext = None
@@ -185,7 +188,7 @@ class SSSP:
             import numpy as np
 
             r = min(int(st.rounds), trace_cap)
-            raw = trace.view(-1, 8)[:r].cpu().numpy()
+            raw = trace.view(-1, ROUND_WORDS)[:r].cpu().numpy()
             tr = np.zeros(r, dtype=[(f, "<u8" if f == "theta" else "<i8") for f in ROUND_FIELDS])
             for i, f in enumerate(ROUND_FIELDS):
                 tr[f] = raw[:, i].view("<u8") if f == "theta" else raw[:, i]

@@ -30,22 +30,28 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=()) -> str:
+    """Compile every csrc/*.cu into one shared library (defines: tuning variants, e.g. SSSP_ARCS=4)."""
+    if not force and out == OUT and not defines and up_to_date():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", OUT, *sources()]
+    cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", out, *sources()]
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(HERE, "build.log")
+    log = os.path.join(HERE, "build.log" if out == OUT else os.path.basename(out) + ".log")
     with open(log, "w") as f:
         f.write(res.stdout + res.stderr)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    # python build.py [--force] [--out lib.so] [-DNAME=VAL ...]
+    args = sys.argv[1:]
+    out = OUT
+    if "--out" in args:
+        out = os.path.abspath(args[args.index("--out") + 1])
+    build(force="--force" in args, out=out, defines=[a[2:] for a in args if a.startswith("-D")])

@@ -5,6 +5,7 @@
 // Citations: P:n = /root/reference/PAPER.md line n.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -98,20 +99,10 @@ __device__ __forceinline__ int32_t warp_incl_scan(int32_t v) {
 }
 
 // ------------------------------------------------------------------ grid barrier
-// Sense-free arrival counter (the top bit flips once all CTAs arrived): CTA 0 adds
-// 2^31 - (G-1), every other CTA adds 1.  Requires a cooperative launch.
-__device__ __forceinline__ void grid_sync(unsigned* bar) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned inc = (blockIdx.x == 0) ? (0x80000000u - (gridDim.x - 1)) : 1u;
-        __threadfence();
-        unsigned old = atomicAdd(bar, inc);
-        while (((old ^ ld_acquire_u32(bar)) & 0x80000000u) == 0) {
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
+// Requires a cooperative launch.  cooperative_groups' grid sync measured 1.2 us at
+// 296-444 CTAs on B200 vs 1.5-1.9 us for a hand-written arrive/spin counter
+// (scripts/bench_barrier.cu, profiles/bench_barrier_r1.log).
+__device__ __forceinline__ void grid_sync(unsigned* /*unused*/) { cooperative_groups::this_grid().sync(); }
 
 // ------------------------------------------------------------------ sampling (reading R5/R6)
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {

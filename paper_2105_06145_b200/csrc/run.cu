@@ -1,20 +1,29 @@
 // run.cu — the stepping-algorithm round loop (Alg. 1) as ONE persistent
 // cooperative kernel, plus the sssp_* handle API.
 //
-// Per round r (DESIGN.md "Round loop"):
-//   ExtDist   theta_r per policy (Table tab:framework).  BF / Delta* /
-//             Dijkstra: a scalar every CTA derives identically; rho: CTA 0 samples
-//             the queue and radix-selects, then one grid barrier.
-//   Extract   (array LaB-PQ P:1011-1012) one pass over the compacted
-//             queue: ids with delta <= theta have their flag cleared and go to the
-//             frontier with a snapshot of delta (reading R8), binned by degree
-//             into light entries and heavy chunks; the rest are compacted into the
-//             next queue.  Warp ballots + one atomic per warp.        grid barrier
-//   Relax     (Alg. 1 lines 4-6) warps pull work items (32 light
-//             vertices, or one 256-arc chunk of a heavy vertex) from an atomic
-//             counter; per arc: plain L2 load filter, WriteMin = atomicMin.u64
-//             (P:697), on success Update(v) = atomicOr on the flag bitmap, and
-//             the 0->1 winner appends v to the next queue.         grid barrier
+// LaB-PQ of the round loop (DESIGN.md §5 "Queue state"): the membership flag of a
+// vertex lives in the top bit of its delta word (bit 63 set = NOT in Q), the value
+// in the low 63 bits; the queue is a compacted id array (ping-pong per round).
+//   Update(v)   = the WriteMin CAS that lowers the value also clears bit 63; the
+//                 thread whose CAS saw bit 63 set appends v (exactly one append per
+//                 insertion, no duplicates).
+//   Extract(u)  = atomicOr(bit 63): deletes u from Q and returns, atomically, the
+//                 value it is relaxed with (its snapshot key).
+// Because flag and key share one word, a concurrent WriteMin and Extract can never
+// lose an update, so Extract and relax may overlap ("live" rounds, the default).
+//
+// Per round r:
+//   ExtDist  theta_r per policy (Table tab:framework).  rho: every CTA
+//            draws the same counter-based samples into shared memory and radix-
+//            selects the same theta (readings R5/R6) -> no barrier.
+//   Phase A  one pass over the queue (array LaB-PQ P:1011-1012): ids with
+//            key <= theta are extracted; vertices of degree <= kLight are relaxed at
+//            once by the extracting warp (live) or listed (snapshot mode); heavier
+//            ones are cut into kChunk-arc descriptors; the rest of Q is compacted
+//            into the next queue.                                     grid barrier
+//   Phase B  warps stride over the chunk descriptors (and, in snapshot mode, the
+//            light list): per arc c = d_u + w, plain L2 load filter, WriteMin by
+//            CAS, append on insertion.       grid barrier (only if non-empty)
 //   loop while |Q| > 0: |Q_{r+1}| is the next queue's tail counter.
 #include <stdio.h>
 
@@ -26,31 +35,45 @@
 
 namespace sssp {
 
-constexpr int kLightMax = 64;  // out-degree <= kLightMax: relaxed in warp batches of 32 vertices
-constexpr int kChunk = 256;    // heavy vertices are split into chunks of kChunk arcs
-constexpr int kBlock = 512;    // threads per CTA of the round loop
-constexpr int kUnroll = 4;     // arcs per lane in flight
+constexpr uint64_t kTop = 1ull << 63;  // flag bit: set = not in Q
+constexpr uint64_t kVal = kTop - 1;    // value bits of a delta word
+#ifndef SSSP_MIN_BLOCKS
+#define SSSP_MIN_BLOCKS 2
+#endif
+#ifndef SSSP_ARCS
+#define SSSP_ARCS 8
+#endif
+#ifndef SSSP_LIGHT
+#define SSSP_LIGHT 128
+#endif
+constexpr int kBlock = 512;                 // threads per CTA of the round loop
+constexpr int kMinBlocks = SSSP_MIN_BLOCKS; // CTAs per SM the register budget targets
+constexpr int kArcs = SSSP_ARCS;            // arcs per lane in flight
+constexpr int kChunk = 32 * kArcs;     // arcs per heavy-chunk descriptor
+constexpr int kLight = SSSP_LIGHT;     // out-degree <= kLight: relaxed by the extracting warp
+constexpr int kSmemSamples = 4096;     // theta samples held in shared memory (else CTA-0 fallback)
+constexpr int kRankSelect = 256;       // s <= this: select by rank counting
 
-// A frontier entry: the extracted vertex's snapshot key and its CSR row.
-struct __align__(16) FEntry {
+// A vertex (or a piece of one) to relax: snapshot key and a CSR arc range.
+struct __align__(16) Desc {
     uint64_t d;
     int32_t beg;
-    int32_t deg;
+    int32_t len;
 };
 
 struct __align__(128) RoundCnt {
-    int32_t tail;   // next-queue write cursor (remaining ids, then appended ids)
-    int32_t nlight; // light frontier entries
-    int32_t work;   // relax work-item counter
-    int32_t pad0;
-    unsigned long long heavy_pack;  // (#heavy << 32) | #chunks
-    unsigned long long minrem;      // min key among ids kept in Q by Extract
-    unsigned long long minsucc;     // min successful WriteMin value
-    unsigned long long theta;
-    unsigned long long edges;       // STATS
-    unsigned long long succ;        // STATS
-    unsigned long long inserts;     // STATS
-    unsigned long long pad1[6];
+    int32_t tail;    // next-queue write cursor (remaining ids, then inserted ids)
+    int32_t nlight;  // snapshot mode: light frontier entries
+    int32_t nchunk;  // heavy chunk descriptors
+    int32_t nheavy;  // STATS: heavy vertices
+    unsigned long long minrem;   // min key among ids Extract kept in Q
+    unsigned long long minsucc;  // min successful WriteMin value
+    unsigned long long theta;    // CTA-0 fallback theta
+    unsigned long long fsize;    // STATS: extracted
+    unsigned long long edges;    // STATS: arcs of extracted vertices
+    unsigned long long succ;     // STATS: successful WriteMins
+    unsigned long long inserts;  // STATS: ids appended by relax
+    unsigned long long pad[5];
 };
 
 struct __align__(128) Ctrl {
@@ -72,13 +95,10 @@ struct RunParams {
     const int32_t* __restrict__ idx;
     const uint32_t* __restrict__ w;
     uint64_t* dist;
-    uint32_t* bm;
     int32_t* q0;
     int32_t* q1;
-    FEntry* light;
-    FEntry* heavy;
-    int32_t* heavy_cb;
-    int32_t* chunk_owner;
+    Desc* light;
+    Desc* chunks;
     uint64_t* samples;
     Ctrl* ctrl;
     uint64_t param;
@@ -93,268 +113,438 @@ struct RunParams {
 __device__ __forceinline__ void reset_cnt(RoundCnt* c) {
     c->tail = 0;
     c->nlight = 0;
-    c->work = 0;
-    c->heavy_pack = 0;
+    c->nchunk = 0;
+    c->nheavy = 0;
     c->minrem = kInf;
     c->minsucc = kInf;
     c->theta = 0;
+    c->fsize = 0;
     c->edges = 0;
     c->succ = 0;
     c->inserts = 0;
 }
 
-__device__ __forceinline__ FEntry ld_entry(const FEntry* p) {
-    uint4 v = __ldcg((const uint4*)p);
-    FEntry e;
+__device__ __forceinline__ Desc ld_desc(const Desc* p) {
+    const uint4 v = __ldcg((const uint4*)p);
+    Desc e;
     e.d = ((uint64_t)v.y << 32) | v.x;
     e.beg = (int32_t)v.z;
-    e.deg = (int32_t)v.w;
+    e.len = (int32_t)v.w;
     return e;
 }
-__device__ __forceinline__ void st_entry(FEntry* p, uint64_t d, int32_t beg, int32_t deg) {
-    uint4 v = make_uint4((uint32_t)d, (uint32_t)(d >> 32), (uint32_t)beg, (uint32_t)deg);
-    __stcg((uint4*)p, v);
+__device__ __forceinline__ void st_desc(Desc* p, uint64_t d, int32_t beg, int32_t len) {
+    __stcg((uint4*)p, make_uint4((uint32_t)d, (uint32_t)(d >> 32), (uint32_t)beg, (uint32_t)len));
 }
+__device__ __forceinline__ void st_desc_smem(Desc* p, uint64_t d, int32_t beg, int32_t len) {
+    p->d = d;
+    p->beg = beg;
+    p->len = len;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Global warp rank, CTA-minor: consecutive work items land on different SMs, so a
+// small round is spread over the whole GPU instead of the first few CTAs.
+__device__ __forceinline__ int64_t warp_rank() { return (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x; }
 
 __host__ __device__ constexpr bool uses_min(int pol) { return pol == SSSP_DELTA || pol == SSSP_DIJKSTRA; }
 
-// --------------------------------------------------------------------- Extract
-template <int POL, bool STATS>
-__device__ __forceinline__ void extract_phase(const RunParams& p, const int32_t* __restrict__ qcur,
-                                              int32_t* __restrict__ qnext, int32_t q, uint64_t theta, RoundCnt* C) {
-    const int lane = lane_id();
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    uint64_t minrem = kInf;
-    uint64_t edges = 0;
-    for (int64_t base = gw * 32; base < q; base += nwarps * 32) {
-        const int64_t i = base + lane;
-        const bool valid = i < q;
-        const int32_t id = valid ? ld_cg_i32(qcur + i) : 0;
-        const uint64_t d = valid ? ld_cg_u64(p.dist + id) : kInf;
-        const bool take = valid && d <= theta;
-        const bool rem = valid && !take;
-        int32_t beg = 0, deg = 0;
-        if (take) {
-            beg = __ldg(p.off + id);
-            deg = __ldg(p.off + id + 1) - beg;
-            atomicAnd(p.bm + (id >> 5), ~(1u << (id & 31)));  // delete from Q
-            if (p.ext_count) atomicAdd(p.ext_count + id, 1);
-        }
-        // ids that stay in Q are compacted into the next queue
-        const int32_t rs = warp_append_slot(rem, &C->tail);
-        if (rem) qnext[rs] = id;
-        if (uses_min(POL) && rem) minrem = d < minrem ? d : minrem;
-        // light frontier entries
-        const bool heavy = take && deg > kLightMax;
-        const bool light = take && !heavy;
-        const int32_t ls = warp_append_slot(light, &C->nlight);
-        if (light) st_entry(p.light + ls, d, beg, deg);
-        // heavy vertices: one packed atomic gives (slot, first chunk) consistently
-        const uint32_t hm = __ballot_sync(kFull, heavy);
-        if (hm) {
-            const int32_t nch = heavy ? (deg + kChunk - 1) / kChunk : 0;
-            const int32_t incl = warp_incl_scan(nch);
-            const int32_t tot = __shfl_sync(kFull, incl, 31);
-            unsigned long long old = 0;
-            if (lane == 0) old = atomicAdd(&C->heavy_pack, ((unsigned long long)__popc(hm) << 32) | (unsigned)tot);
-            old = __shfl_sync(kFull, old, 0);
-            if (heavy) {
-                const int32_t slot = (int32_t)(old >> 32) + __popc(hm & lanemask_lt());
-                const int32_t cb = (int32_t)(old & 0xFFFFFFFFu) + incl - nch;
-                st_entry(p.heavy + slot, d, beg, deg);
-                __stcg(p.heavy_cb + slot, cb);
-                for (int32_t j = 0; j < nch; j++) __stcg(p.chunk_owner + cb + j, slot);
-            }
-        }
-        if (STATS && take) edges += (uint64_t)deg;
-    }
-    if (uses_min(POL)) {
-        minrem = warp_min_u64(minrem);
-        if (lane == 0 && minrem != kInf) atomicMin(&C->minrem, (unsigned long long)minrem);
-    }
-    if (STATS) {
-        edges = warp_sum(edges);
-        if (lane == 0 && edges) atomicAdd(&C->edges, (unsigned long long)edges);
-    }
-}
+// --------------------------------------------------------------------- per-warp staging
+// Appends to the next queue, and light vertices waiting to be relaxed, are staged in a
+// warp-private shared-memory buffer: one global atomicAdd per ~kQBuf appended ids
+// instead of one per warp step, and the flush is a coalesced store.
+constexpr int kWarps = kBlock / 32;
+constexpr int kEnt = 4;     // queue entries per lane per Extract step
+constexpr int kQBuf = 256;  // staged queue ids per warp (>= 32 * kArcs)
+constexpr int kLBuf = 32 * kEnt + 32;  // staged light vertices per warp
+static_assert(32 * kArcs <= kQBuf, "one relax step must fit the stage");
 
-// --------------------------------------------------------------------- Relax
-struct RelaxAcc {
-    uint64_t minsucc = kInf;
-    uint64_t succ = 0;
-    uint64_t inserts = 0;
+struct WarpStage {
+    Desc light[kLBuf];
+    int32_t q[kQBuf];
 };
 
-// WriteMin(delta[v], c) and, on success, Q.Update(v) (Alg. 1 lines 5-6).
-// Returns true iff this lane must append v to the queue (its flag went 0 -> 1).
+struct Acc {
+    uint64_t minsucc = kInf;
+    uint32_t succ = 0;
+    uint32_t inserts = 0;
+};
+
+struct Warp {  // per-warp working state (qn, ln are warp-uniform)
+    WarpStage* st;
+    int32_t* qnext;
+    RoundCnt* C;
+    int32_t qn;
+    int32_t ln;
+    Acc acc;
+};
+
+__device__ __forceinline__ void wq_flush(Warp& W) {
+    if (W.qn == 0) return;
+    __syncwarp();
+    int32_t base = 0;
+    if (lane_id() == 0) base = atomicAdd(&W.C->tail, W.qn);
+    base = __shfl_sync(kFull, base, 0);
+    for (int32_t i = lane_id(); i < W.qn; i += 32) W.qnext[base + i] = W.st->q[i];
+    __syncwarp();
+    W.qn = 0;
+}
+
+// stage the lanes' ids with pred (one id per lane)
+__device__ __forceinline__ void wq_push1(Warp& W, bool pred, int32_t id) {
+    const uint32_t mask = __ballot_sync(kFull, pred);
+    if (!mask) return;
+    const int32_t cnt = __popc(mask);
+    if (W.qn + cnt > kQBuf) wq_flush(W);
+    if (pred) W.st->q[W.qn + __popc(mask & lanemask_lt())] = id;
+    W.qn += cnt;
+}
+
+// --------------------------------------------------------------------- relax
+// WriteMin(delta[v], c) on the packed word, given a prior read `w`.
+// Returns true iff this lane inserted v into Q (its flag bit was set) and must append it.
 template <int POL, bool STATS>
-__device__ __forceinline__ bool relax_arc(const RunParams& p, int32_t v, uint64_t c, RelaxAcc& acc) {
-    if (c < ld_cg_u64(p.dist + v)) {  // plain-load filter: most candidates lose
-        const uint64_t old = atomic_min_u64(p.dist + v, c);
-        if (c < old) {
+__device__ __forceinline__ bool write_min(uint64_t* dist, int32_t v, uint64_t c, uint64_t w, Acc& acc) {
+    while ((w & kVal) > c) {
+        const uint64_t old = atomicCAS((unsigned long long*)(dist + v), (unsigned long long)w, (unsigned long long)c);
+        if (old == w) {
             if (STATS) acc.succ++;
             if (uses_min(POL)) acc.minsucc = c < acc.minsucc ? c : acc.minsucc;
-            const uint32_t bit = 1u << (v & 31);
-            return !(atomicOr(p.bm + (v >> 5), bit) & bit);
+            return (w & kTop) != 0;
         }
+        w = old;
     }
     return false;
 }
 
-// Append the lanes' flagged ids (up to kUnroll per lane) with one atomic per warp.
-__device__ __forceinline__ void warp_append_many(const int32_t (&v)[kUnroll], const bool (&app)[kUnroll],
-                                                 int32_t* cursor, int32_t* out, RelaxAcc& acc, bool stats) {
-    int32_t cnt = 0;
+// Relax kArcs arcs per lane (v < 0 = empty slot): filter loads, WriteMins, stage the
+// inserted ids (Alg. 1 lines 5-6).
+template <int POL, bool STATS>
+__device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&v)[kArcs], const uint64_t (&c)[kArcs],
+                                            Warp& W) {
+    uint64_t cur[kArcs];
 #pragma unroll
-    for (int t = 0; t < kUnroll; t++) cnt += app[t];
-    const uint32_t any = __ballot_sync(kFull, cnt != 0);
-    if (!any) return;
+    for (int t = 0; t < kArcs; t++) cur[t] = v[t] >= 0 ? ld_cg_u64(p.dist + v[t]) : 0ull;
+    int32_t cnt = 0;
+    bool app[kArcs];
+#pragma unroll
+    for (int t = 0; t < kArcs; t++) {
+        app[t] = v[t] >= 0 && write_min<POL, STATS>(p.dist, v[t], c[t], cur[t], W.acc);
+        cnt += app[t];
+    }
+    if (!__any_sync(kFull, cnt != 0)) return;
     const int32_t incl = warp_incl_scan(cnt);
     const int32_t tot = __shfl_sync(kFull, incl, 31);
-    int32_t base = 0;
-    if (lane_id() == 0) base = atomicAdd(cursor, tot);
-    base = __shfl_sync(kFull, base, 0);
-    int32_t pos = base + incl - cnt;
+    if (W.qn + tot > kQBuf) wq_flush(W);
+    int32_t pos = W.qn + incl - cnt;
 #pragma unroll
-    for (int t = 0; t < kUnroll; t++)
-        if (app[t]) out[pos++] = v[t];
-    if (stats) acc.inserts += cnt;
+    for (int t = 0; t < kArcs; t++)
+        if (app[t]) W.st->q[pos++] = v[t];
+    W.qn += tot;
+    if (STATS) W.acc.inserts += cnt;
 }
 
-// Arcs [b, e) of one vertex with snapshot key d, all lanes of the warp.
+// One chunk: arcs [beg, beg+len) of a vertex with key d, len <= kChunk.  Lane-strided
+// so every load instruction of the warp reads 128 contiguous bytes.
 template <int POL, bool STATS>
-__device__ __forceinline__ void relax_row(const RunParams& p, uint64_t d, int32_t b, int32_t e, int32_t* qnext,
-                                          RoundCnt* C, RelaxAcc& acc) {
+__device__ __forceinline__ void relax_chunk(const RunParams& p, uint64_t d, int32_t beg, int32_t len, Warp& W) {
     const int lane = lane_id();
-    for (int32_t base = b; base < e; base += 32 * kUnroll) {
-        int32_t v[kUnroll];
-        uint32_t wt[kUnroll];
-        bool app[kUnroll];
+    int32_t v[kArcs];
+    uint64_t c[kArcs];
 #pragma unroll
-        for (int t = 0; t < kUnroll; t++) {
-            const int32_t k = base + t * 32 + lane;
-            v[t] = k < e ? ld_stream_i32(p.idx + k) : -1;
-            wt[t] = k < e ? ld_stream_u32(p.w + k) : 0u;
-        }
-#pragma unroll
-        for (int t = 0; t < kUnroll; t++) app[t] = v[t] >= 0 && relax_arc<POL, STATS>(p, v[t], d + wt[t], acc);
-        warp_append_many(v, app, &C->tail, qnext, acc, STATS);
+    for (int t = 0; t < kArcs; t++) {
+        const int32_t k = t * 32 + lane;
+        v[t] = k < len ? ld_stream_i32(p.idx + beg + k) : -1;
+        c[t] = d + (k < len ? ld_stream_u32(p.w + beg + k) : 0u);
     }
+    relax_slots<POL, STATS>(p, v, c, W);
 }
 
-// 32 light frontier entries: the warp walks their concatenated arc lists.
+// Up to 32 vertices, one per lane (deg = 0 for none): the warp walks their
+// concatenated arc lists; arc e belongs to the largest lane o with excl[o] <= e.
 template <int POL, bool STATS>
-__device__ __forceinline__ void relax_light_batch(const RunParams& p, int32_t batch, int32_t nl, int32_t* qnext,
-                                                  RoundCnt* C, RelaxAcc& acc) {
+__device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, int32_t beg, int32_t deg, Warp& W) {
     const int lane = lane_id();
-    const int32_t j = batch * 32 + lane;
-    FEntry me;
-    if (j < nl) {
-        me = ld_entry(p.light + j);
-    } else {
-        me.d = 0;
-        me.beg = 0;
-        me.deg = 0;
-    }
-    const int32_t incl = warp_incl_scan(me.deg);
+    const int32_t incl = warp_incl_scan(deg);
     const int32_t total = __shfl_sync(kFull, incl, 31);
-    const int32_t excl = incl - me.deg;
-    for (int32_t base = 0; base < total; base += 32 * kUnroll) {
-        int32_t v[kUnroll];
-        uint32_t wt[kUnroll];
-        uint64_t dd[kUnroll];
-        bool app[kUnroll];
+    const int32_t excl = incl - deg;
+    const int32_t rowbase = beg - excl;  // CSR position of concatenated arc e of this lane = rowbase + e
+    for (int32_t s0 = 0; s0 < total; s0 += 32 * kArcs) {
+        int32_t v[kArcs];
+        uint64_t c[kArcs];
 #pragma unroll
-        for (int t = 0; t < kUnroll; t++) {
-            const int32_t eidx = base + t * 32 + lane;
-            // owner = largest lane o with excl[o] <= eidx (binary search over lanes)
+        for (int t = 0; t < kArcs; t++) {
+            const int32_t e = s0 + t * 32 + lane;
             int32_t o = 0;
 #pragma unroll
             for (int step = 16; step > 0; step >>= 1) {
                 const int32_t x = __shfl_sync(kFull, excl, o + step);
-                if (x <= eidx) o += step;
+                if (x <= e) o += step;
             }
-            const int32_t ob = __shfl_sync(kFull, me.beg, o);
-            const int32_t oe = __shfl_sync(kFull, excl, o);
-            dd[t] = __shfl_sync(kFull, me.d, o);
-            const bool ok = eidx < total;
-            const int32_t k = ob + (eidx - oe);
-            v[t] = ok ? ld_stream_i32(p.idx + k) : -1;
-            wt[t] = ok ? ld_stream_u32(p.w + k) : 0u;
+            const int32_t rb = __shfl_sync(kFull, rowbase, o);
+            const uint64_t od = __shfl_sync(kFull, d, o);
+            const bool ok = e < total;
+            v[t] = ok ? ld_stream_i32(p.idx + rb + e) : -1;
+            c[t] = od + (ok ? ld_stream_u32(p.w + rb + e) : 0u);
         }
-#pragma unroll
-        for (int t = 0; t < kUnroll; t++) app[t] = v[t] >= 0 && relax_arc<POL, STATS>(p, v[t], dd[t] + wt[t], acc);
-        warp_append_many(v, app, &C->tail, qnext, acc, STATS);
+        relax_slots<POL, STATS>(p, v, c, W);
+    }
+}
+
+// Stage light vertices (live mode); light_relax_full relaxes them 32 at a time.
+__device__ __forceinline__ void light_stage(bool pred, uint64_t d, int32_t beg, int32_t deg, Warp& W) {
+    const uint32_t mask = __ballot_sync(kFull, pred);
+    if (!mask) return;
+    if (pred) st_desc_smem(&W.st->light[W.ln + __popc(mask & lanemask_lt())], d, beg, deg);
+    W.ln += __popc(mask);
+}
+
+template <int POL, bool STATS>
+__device__ __forceinline__ void light_relax_full(const RunParams& p, Warp& W) {
+    const int lane = lane_id();
+    int32_t done = 0;
+    while (W.ln - done >= 32) {
+        __syncwarp();
+        const Desc e = W.st->light[done + lane];
+        done += 32;
+        relax_vertices<POL, STATS>(p, e.d, e.beg, e.len, W);
+    }
+    if (done) {  // move the remainder (< 32) to the front
+        __syncwarp();
+        const bool mv = lane < W.ln - done;
+        Desc t;
+        if (mv) t = W.st->light[done + lane];
+        __syncwarp();
+        if (mv) W.st->light[lane] = t;
+        __syncwarp();
+        W.ln -= done;
     }
 }
 
 template <int POL, bool STATS>
-__device__ __forceinline__ void relax_phase(const RunParams& p, int32_t* __restrict__ qnext, RoundCnt* C) {
+__device__ __forceinline__ void light_drain(const RunParams& p, Warp& W) {
+    if (W.ln == 0) return;
+    __syncwarp();
     const int lane = lane_id();
-    const int32_t nl = ld_volatile_i32(&C->nlight);
-    const unsigned long long hp = ld_volatile_u64((const uint64_t*)&C->heavy_pack);
-    const int32_t nchunks = (int32_t)(hp & 0xFFFFFFFFull);
-    const int32_t nbatch = (nl + 31) / 32;
-    const int32_t total = nbatch + nchunks;
-    RelaxAcc acc;
-    for (;;) {
-        int32_t item = 0;
-        if (lane == 0) item = atomicAdd(&C->work, 1);
-        item = __shfl_sync(kFull, item, 0);
-        if (item >= total) break;
-        if (item < nbatch) {
-            relax_light_batch<POL, STATS>(p, item, nl, qnext, C, acc);
-        } else {
-            const int32_t c = item - nbatch;
-            const int32_t o = ld_cg_i32(p.chunk_owner + c);
-            const FEntry e = ld_entry(p.heavy + o);
-            const int32_t start = (c - ld_cg_i32(p.heavy_cb + o)) * kChunk;
-            const int32_t end = min(start + kChunk, e.deg);
-            relax_row<POL, STATS>(p, e.d, e.beg + start, e.beg + end, qnext, C, acc);
+    Desc e;
+    e.d = 0;
+    e.beg = 0;
+    e.len = 0;
+    if (lane < W.ln) e = W.st->light[lane];
+    __syncwarp();
+    W.ln = 0;
+    relax_vertices<POL, STATS>(p, e.d, e.beg, e.len, W);
+}
+
+// Cut the heavy lanes' vertices into kChunk-arc descriptors; one atomic per warp.
+__device__ __forceinline__ void emit_chunks(const RunParams& p, bool heavy, uint64_t d, int32_t beg, int32_t deg,
+                                            RoundCnt* C, bool stats) {
+    const uint32_t hm = __ballot_sync(kFull, heavy);
+    if (!hm) return;
+    const int lane = lane_id();
+    const int32_t nch = heavy ? (deg + kChunk - 1) / kChunk : 0;
+    const int32_t incl = warp_incl_scan(nch);
+    const int32_t tot = __shfl_sync(kFull, incl, 31);
+    const int32_t excl = incl - nch;
+    int32_t base = 0;
+    if (lane == 0) {
+        base = atomicAdd(&C->nchunk, tot);
+        if (stats) atomicAdd(&C->nheavy, __popc(hm));
+    }
+    base = __shfl_sync(kFull, base, 0);
+    for (int32_t j0 = 0; j0 < tot; j0 += 32) {
+        const int32_t j = j0 + lane;
+        int32_t o = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int32_t x = __shfl_sync(kFull, excl, o + step);
+            if (x <= j) o += step;
+        }
+        const int32_t ob = __shfl_sync(kFull, beg, o);
+        const int32_t oe = __shfl_sync(kFull, excl, o);
+        const int32_t od = __shfl_sync(kFull, deg, o);
+        const uint64_t odd = __shfl_sync(kFull, d, o);
+        if (j < tot) {
+            const int32_t k = (j - oe) * kChunk;
+            st_desc(p.chunks + base + j, odd, ob + k, min(kChunk, od - k));
         }
     }
+}
+
+// --------------------------------------------------------------------- phase A
+// Extract(theta): kEnt queue entries per lane per step, all loads issued together.
+template <int POL, bool STATS, bool SNAP>
+__device__ __forceinline__ void phase_a(const RunParams& p, const int32_t* __restrict__ qcur, int32_t q,
+                                        uint64_t theta, Warp& W) {
+    const int lane = lane_id();
+    const int64_t gw = warp_rank();
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    uint64_t minrem = kInf, fs = 0, edges = 0;
+    // kEnt entries per lane only when every warp gets at least two such steps; small
+    // queues are spread one entry per lane so that more warps share the round
+    const int ent = (int64_t)q >= nwarps * (64 * kEnt) ? kEnt : 1;
+    for (int64_t base = gw * (32 * ent); base < q; base += nwarps * (32 * ent)) {
+        int32_t id[kEnt];
+        uint64_t val[kEnt];
+#pragma unroll
+        for (int e = 0; e < kEnt; e++) {
+            const int64_t i = base + e * 32 + lane;
+            id[e] = (e < ent && i < q) ? ld_cg_i32(qcur + i) : -1;
+        }
+#pragma unroll
+        for (int e = 0; e < kEnt; e++) val[e] = id[e] >= 0 ? (ld_cg_u64(p.dist + id[e]) & kVal) : kVal;
+        int32_t beg[kEnt], deg[kEnt];
+#pragma unroll
+        for (int e = 0; e < kEnt; e++) {
+            beg[e] = 0;
+            deg[e] = 0;
+            if (id[e] >= 0 && val[e] <= theta) {
+                // delete u from Q; the returned word is u's key at deletion (<= val)
+                val[e] = atomicOr((unsigned long long*)(p.dist + id[e]), (unsigned long long)kTop) & kVal;
+                beg[e] = __ldg(p.off + id[e]);
+                deg[e] = __ldg(p.off + id[e] + 1) - beg[e];
+                if (p.ext_count) atomicAdd(p.ext_count + id[e], 1);
+            } else if (id[e] >= 0) {
+                deg[e] = -1;  // stays in Q
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < kEnt; e++) {
+            const bool rem = deg[e] < 0;
+            const bool take = id[e] >= 0 && !rem;
+            wq_push1(W, rem, id[e]);
+            if (uses_min(POL) && rem) minrem = val[e] < minrem ? val[e] : minrem;
+            if (STATS && take) {
+                fs += 1;
+                edges += (uint64_t)deg[e];
+            }
+            const bool heavy = take && deg[e] > kLight;
+            const bool light = take && deg[e] > 0 && !heavy;
+            emit_chunks(p, heavy, val[e], beg[e], deg[e], W.C, STATS);
+            if (SNAP) {
+                const int32_t ls = warp_append_slot(light, &W.C->nlight);
+                if (light) st_desc(p.light + ls, val[e], beg[e], deg[e]);
+            } else {
+                light_stage(light, val[e], beg[e], deg[e], W);
+            }
+        }
+        if (!SNAP) light_relax_full<POL, STATS>(p, W);
+    }
+    if (!SNAP) light_drain<POL, STATS>(p, W);
     if (uses_min(POL)) {
-        const uint64_t m = warp_min_u64(acc.minsucc);
-        if (lane == 0 && m != kInf) atomicMin(&C->minsucc, (unsigned long long)m);
+        minrem = warp_min_u64(minrem);
+        if (lane == 0 && minrem != kInf) atomicMin(&W.C->minrem, (unsigned long long)minrem);
     }
     if (STATS) {
-        const uint64_t s = warp_sum(acc.succ), ins = warp_sum(acc.inserts);
-        if (lane == 0 && s) atomicAdd(&C->succ, (unsigned long long)s);
-        if (lane == 0 && ins) atomicAdd(&C->inserts, (unsigned long long)ins);
+        fs = warp_sum(fs);
+        edges = warp_sum(edges);
+        if (lane == 0 && fs) atomicAdd(&W.C->fsize, (unsigned long long)fs);
+        if (lane == 0 && edges) atomicAdd(&W.C->edges, (unsigned long long)edges);
     }
+}
+
+// --------------------------------------------------------------------- phase B
+template <int POL, bool STATS, bool SNAP>
+__device__ __forceinline__ void phase_b(const RunParams& p, int32_t nl, int32_t nc, Warp& W) {
+    const int lane = lane_id();
+    const int64_t gw = warp_rank();
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nb = SNAP ? ((int64_t)nl + 31) / 32 : 0;
+    const int64_t total = nb + nc;
+    int64_t item = gw;
+    Desc nxt;
+    if (item >= nb && item < total) nxt = ld_desc(p.chunks + (item - nb));
+    for (; item < total; item += nwarps) {
+        if (SNAP && item < nb) {
+            const int64_t j = item * 32 + lane;
+            Desc e;
+            if (j < nl) {
+                e = ld_desc(p.light + j);
+            } else {
+                e.d = 0;
+                e.beg = 0;
+                e.len = 0;
+            }
+            relax_vertices<POL, STATS>(p, e.d, e.beg, e.len, W);
+            if (item + nwarps >= nb && item + nwarps < total) nxt = ld_desc(p.chunks + (item + nwarps - nb));
+        } else {
+            const Desc e = nxt;
+            if (item + nwarps < total) nxt = ld_desc(p.chunks + (item + nwarps - nb));  // prefetch
+            relax_chunk<POL, STATS>(p, e.d, e.beg, e.len, W);
+        }
+    }
+}
+
+template <int POL, bool STATS>
+__device__ __forceinline__ void flush_acc(Warp& W) {
+    wq_flush(W);
+    if (uses_min(POL)) {
+        const uint64_t mn = warp_min_u64(W.acc.minsucc);
+        if (lane_id() == 0 && mn != kInf) atomicMin(&W.C->minsucc, (unsigned long long)mn);
+    }
+    if (STATS) {
+        const uint32_t s = warp_sum(W.acc.succ), ins = warp_sum(W.acc.inserts);
+        if (lane_id() == 0 && s) atomicAdd(&W.C->succ, (unsigned long long)s);
+        if (lane_id() == 0 && ins) atomicAdd(&W.C->inserts, (unsigned long long)ins);
+    }
+    W.acc = Acc();
 }
 
 // --------------------------------------------------------------------- ExtDist for rho
-__device__ uint64_t cta_rho_theta(const RunParams& p, const int32_t* qcur, int32_t q, uint64_t rho, int64_t round,
-                                  SelectSmem& sm) {
-    if (p.flags & SSSP_RUN_RHO_EXACT) {
-        return cta_kth_smallest(QueueKey{qcur, p.dist}, q, rho, sm);
-    }
-    const uint64_t s = sample_count((uint64_t)q, rho);
-    for (uint64_t j = threadIdx.x; j < s; j += blockDim.x) {
-        const uint64_t r = splitmix64(p.seed ^ splitmix64(((uint64_t)round << 32) | j));
-        p.samples[j] = ld_cg_u64(p.dist + ld_cg_i32(qcur + (int64_t)(r % (uint64_t)q)));
+struct SmemKey {
+    const uint64_t* a;
+    __device__ uint64_t operator()(int64_t i) const { return a[i]; }
+};
+struct QueueVal {  // value of the i-th queued id (flag bit masked off), read through L2
+    const int32_t* queue;
+    const uint64_t* dist;
+    __device__ uint64_t operator()(int64_t i) const { return ld_cg_u64(dist + ld_cg_i32(queue + i)) & kVal; }
+};
+
+__device__ __forceinline__ uint64_t sample_index(uint64_t seed, int64_t round, uint64_t j, uint64_t q) {
+    return splitmix64(seed ^ splitmix64(((uint64_t)round << 32) | j)) % q;
+}
+
+// k-th smallest (1-based) of s <= blockDim keys in shared memory by rank counting:
+// the key x with #{< x} < k <= #{<= x}.  One pass of broadcast reads, two barriers.
+__device__ __forceinline__ uint64_t cta_kth_by_rank(const uint64_t* keys, int s, uint64_t k, SelectSmem& sm) {
+    const int tid = threadIdx.x;
+    if (tid < s) {
+        const uint64_t x = keys[tid];
+        uint32_t lt = 0, le = 0;
+        for (int j = 0; j < s; j++) {
+            const uint64_t y = keys[j];
+            lt += y < x;
+            le += y <= x;
+        }
+        if (lt < k && k <= le) sm.bcast[0] = x;  // every writer writes the same value
     }
     __syncthreads();
-    uint64_t k = (rho * s + (uint64_t)q - 1) / (uint64_t)q;
-    k = k < 1 ? 1 : (k > s ? s : k);
-    return cta_kth_smallest(ArrayKey{p.samples}, (int64_t)s, k, sm);
+    const uint64_t th = sm.bcast[0];
+    __syncthreads();
+    return th;
 }
 
 // --------------------------------------------------------------------- the round loop
-template <int POL, bool STATS>
-__global__ void __launch_bounds__(kBlock) sssp_round_loop(RunParams p) {
-    __shared__ SelectSmem sm;
+template <int POL, bool STATS, bool SNAP>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpStage* stage = (WarpStage*)smem_raw;                            // [kWarps]
+    uint64_t* s_keys = (uint64_t*)(smem_raw + kWarps * sizeof(WarpStage)); // [kSmemSamples]
+    SelectSmem& sm = *(SelectSmem*)(s_keys + kSmemSamples);
     Ctrl* ctrl = p.ctrl;
+    Warp W;
+    W.st = stage + (threadIdx.x >> 5);
+    W.qn = 0;
+    W.ln = 0;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
 
-    // Alg. 1 lines 1-2: delta[.] = +inf, delta[s] = 0, Q.Update(s)
+    // Alg. 1 lines 1-2: delta[.] = +inf (not in Q), delta[s] = 0 (in Q), queue = {s}
     for (int64_t i = gtid; i < p.n; i += gsize) p.dist[i] = (i == p.source) ? 0ull : kInf;
-    const int64_t nwords = ((int64_t)p.n + 31) >> 5;
-    for (int64_t i = gtid; i < nwords; i += gsize)
-        p.bm[i] = (i == (p.source >> 5)) ? (1u << (p.source & 31)) : 0u;
     if (p.ext_count)
         for (int64_t i = gtid; i < p.n; i += gsize) p.ext_count[i] = 0;
     if (gtid == 0) {
@@ -381,6 +571,8 @@ __global__ void __launch_bounds__(kBlock) sssp_round_loop(RunParams p) {
             if (gtid == 0) ctrl->status = SSSP_ERR_ROUNDS;
             break;
         }
+        uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+        if (STATS && gtid == 0) t0 = globaltimer();
         if (gtid == 0) reset_cnt(&ctrl->cnt[(r + 1) % 3]);
         const int32_t* qcur = (r & 1) ? p.q0 : p.q1;
         int32_t* qnext = (r & 1) ? p.q1 : p.q0;
@@ -392,7 +584,7 @@ __global__ void __launch_bounds__(kBlock) sssp_round_loop(RunParams p) {
         } else if (POL == SSSP_DIJKSTRA || POL == SSSP_DELTA) {
             const uint64_t a = ld_volatile_u64((const uint64_t*)&P->minrem);
             const uint64_t b = ld_volatile_u64((const uint64_t*)&P->minsucc);
-            const uint64_t minq = a < b ? a : b;  // = min_{v in Q} delta[v], exactly
+            const uint64_t minq = a < b ? a : b;  // <= min_{v in Q} delta[v] (exact in snapshot mode)
             if (POL == SSSP_DIJKSTRA) {
                 theta = minq;
             } else {
@@ -406,30 +598,61 @@ __global__ void __launch_bounds__(kBlock) sssp_round_loop(RunParams p) {
             uint64_t rho = p.param;
             if (!(p.flags & SSSP_RUN_NO_WARMUP) && (uint64_t)q > rho && warm < 2) {
                 warm++;
-                rho = rho / 10 ? rho / 10 : 1;
+                rho = rho / 10 ? rho / 10 : 1;  // reading R7
             }
+            const uint64_t s = sample_count((uint64_t)q, rho);
             if ((uint64_t)q <= rho) {
                 theta = kInf;  // |Q| <= rho: extract all
+            } else if (!(p.flags & SSSP_RUN_RHO_EXACT) && s <= (uint64_t)kSmemSamples) {
+                // every CTA draws the same samples and selects the same theta: no barrier
+                for (uint64_t j = threadIdx.x; j < s; j += blockDim.x)
+                    s_keys[j] = ld_cg_u64(p.dist + ld_cg_i32(qcur + sample_index(p.seed, r, j, (uint64_t)q))) & kVal;
+                __syncthreads();
+                uint64_t k = (rho * s + (uint64_t)q - 1) / (uint64_t)q;
+                k = k < 1 ? 1 : (k > s ? s : k);
+                theta = s <= (uint64_t)kRankSelect ? cta_kth_by_rank(s_keys, (int)s, k, sm)
+                                                   : cta_kth_smallest(SmemKey{s_keys}, (int64_t)s, k, sm);
             } else {
                 if (blockIdx.x == 0) {
-                    const uint64_t th = cta_rho_theta(p, qcur, q, rho, r, sm);
+                    uint64_t th;
+                    if (p.flags & SSSP_RUN_RHO_EXACT) {
+                        th = cta_kth_smallest(QueueVal{qcur, p.dist}, q, rho, sm);
+                    } else {
+                        for (uint64_t j = threadIdx.x; j < s; j += blockDim.x)
+                            p.samples[j] =
+                                ld_cg_u64(p.dist + ld_cg_i32(qcur + sample_index(p.seed, r, j, (uint64_t)q))) & kVal;
+                        __syncthreads();
+                        uint64_t k = (rho * s + (uint64_t)q - 1) / (uint64_t)q;
+                        k = k < 1 ? 1 : (k > s ? s : k);
+                        th = cta_kth_smallest(ArrayKey{p.samples}, (int64_t)s, k, sm);
+                    }
                     if (threadIdx.x == 0) C->theta = th;
                 }
                 grid_sync(&ctrl->bar);
                 theta = ld_volatile_u64((const uint64_t*)&C->theta);
             }
         }
+        if (STATS && gtid == 0) t1 = globaltimer();
 
-        // ---- Extract(theta)
-        extract_phase<POL, STATS>(p, qcur, qnext, q, theta, C);
+        // ---- phase A: Extract(theta) (+ light relax in live mode)
+        W.qnext = qnext;
+        W.C = C;
+        phase_a<POL, STATS, SNAP>(p, qcur, q, theta, W);
+        flush_acc<POL, STATS>(W);
         grid_sync(&ctrl->bar);
-        // ---- relax N(F) with WriteMin, Update improved vertices
-        relax_phase<POL, STATS>(p, qnext, C);
-        grid_sync(&ctrl->bar);
+        if (STATS && gtid == 0) t2 = globaltimer();
+        // ---- phase B: heavy chunks (+ light list in snapshot mode)
+        const int32_t nc = ld_volatile_i32(&C->nchunk);
+        const int32_t nl = SNAP ? ld_volatile_i32(&C->nlight) : 0;
+        if (nc + nl > 0) {
+            phase_b<POL, STATS, SNAP>(p, nl, nc, W);
+            flush_acc<POL, STATS>(W);
+            grid_sync(&ctrl->bar);
+        }
+        if (STATS && gtid == 0) t3 = globaltimer();
 
         if (STATS && gtid == 0) {
-            const unsigned long long hp = C->heavy_pack;
-            const int64_t f = (int64_t)C->nlight + (int64_t)(hp >> 32);
+            const int64_t f = (int64_t)C->fsize;
             if (p.trace && r - 1 < p.trace_cap) {
                 sssp_round* t = p.trace + (r - 1);
                 t->qsize = q;
@@ -438,8 +661,12 @@ __global__ void __launch_bounds__(kBlock) sssp_round_loop(RunParams p) {
                 t->inserts = (int64_t)C->inserts;
                 t->succ = (int64_t)C->succ;
                 t->theta = theta;
-                t->nheavy = (int64_t)(hp >> 32);
-                t->reserved = 0;
+                t->nheavy = (int64_t)C->nheavy;
+                t->t_theta_ns = (int64_t)(t1 - t0);
+                t->t_extract_ns = (int64_t)(t2 - t1);
+                t->t_relax_ns = (int64_t)(t3 - t2);
+                t->reserved0 = C->nchunk;
+                t->reserved1 = 0;
             }
             ctrl->tot_extracted += f;
             ctrl->tot_edges += (int64_t)C->edges;
@@ -451,6 +678,11 @@ __global__ void __launch_bounds__(kBlock) sssp_round_loop(RunParams p) {
         }
     }
     if (gtid == 0) ctrl->rounds = r - 1;
+    // S6 output: strip the flag bit (every reached vertex was extracted; INF stays INF)
+    for (int64_t i = gtid; i < p.n; i += gsize) {
+        const uint64_t x = __ldcg((const unsigned long long*)(p.dist + i));
+        if (x != kInf && (x & kTop)) p.dist[i] = x & kVal;
+    }
 }
 
 // --------------------------------------------------------------------- CSR validation
@@ -487,17 +719,15 @@ struct sssp_handle {
     int device;
     cudaEvent_t ev[2];
     int num_sms;
-    int grid[4][2];
+    int grid[4][2][2];
 };
 
 namespace {
 
 struct Layout {
     uint64_t* dist;
-    uint32_t* bm;
     int32_t *q0, *q1;
-    FEntry *light, *heavy;
-    int32_t *heavy_cb, *chunk_owner;
+    Desc *light, *chunks;
     uint64_t* samples;
     Ctrl* ctrl;
     int32_t* err;
@@ -507,18 +737,15 @@ struct Layout {
 Layout carve(void* base, int32_t n, int64_t m) {
     Carver c(base);
     Layout L;
-    const int64_t hcap = std::min<int64_t>(n, m / (kLightMax + 1)) + 1;
-    const int64_t ccap = m / kChunk + hcap + 1;
+    // chunks per round <= sum over heavy extracted vertices of ceil(deg/kChunk)
+    const int64_t ccap = m / kChunk + std::min<int64_t>(n, m / (kLight + 1)) + 1;
     L.ctrl = c.take<Ctrl>(1);
     L.err = c.take<int32_t>(32);
     L.dist = c.take<uint64_t>(n);
-    L.bm = c.take<uint32_t>(((size_t)n + 31) / 32);
     L.q0 = c.take<int32_t>(n);
     L.q1 = c.take<int32_t>(n);
-    L.light = c.take<FEntry>(n);
-    L.heavy = c.take<FEntry>(hcap);
-    L.heavy_cb = c.take<int32_t>(hcap);
-    L.chunk_owner = c.take<int32_t>(ccap);
+    L.light = c.take<Desc>(n);
+    L.chunks = c.take<Desc>(ccap);
     L.samples = c.take<uint64_t>(kMaxSamples);
     L.bytes = align_up(c.off, 256);
     return L;
@@ -526,14 +753,20 @@ Layout carve(void* base, int32_t n, int64_t m) {
 
 typedef void (*KernelFn)(RunParams);
 
-KernelFn kernel_for(int pol, bool stats) {
+constexpr size_t kSmemBytes = kWarps * sizeof(WarpStage) + kSmemSamples * sizeof(uint64_t) + sizeof(SelectSmem);
+
+template <int POL>
+KernelFn kernel_for_pol(bool stats, bool snap) {
+    if (stats) return snap ? sssp_round_loop<POL, true, true> : sssp_round_loop<POL, true, false>;
+    return snap ? sssp_round_loop<POL, false, true> : sssp_round_loop<POL, false, false>;
+}
+
+KernelFn kernel_for(int pol, bool stats, bool snap) {
     switch (pol) {
-        case SSSP_RHO: return stats ? sssp_round_loop<SSSP_RHO, true> : sssp_round_loop<SSSP_RHO, false>;
-        case SSSP_DELTA: return stats ? sssp_round_loop<SSSP_DELTA, true> : sssp_round_loop<SSSP_DELTA, false>;
-        case SSSP_BELLMAN_FORD:
-            return stats ? sssp_round_loop<SSSP_BELLMAN_FORD, true> : sssp_round_loop<SSSP_BELLMAN_FORD, false>;
-        case SSSP_DIJKSTRA:
-            return stats ? sssp_round_loop<SSSP_DIJKSTRA, true> : sssp_round_loop<SSSP_DIJKSTRA, false>;
+        case SSSP_RHO: return kernel_for_pol<SSSP_RHO>(stats, snap);
+        case SSSP_DELTA: return kernel_for_pol<SSSP_DELTA>(stats, snap);
+        case SSSP_BELLMAN_FORD: return kernel_for_pol<SSSP_BELLMAN_FORD>(stats, snap);
+        case SSSP_DIJKSTRA: return kernel_for_pol<SSSP_DIJKSTRA>(stats, snap);
     }
     return nullptr;
 }
@@ -591,26 +824,28 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
     b.off = d_offsets;
     b.idx = d_indices;
     b.w = d_weights;
-    b.bm = L.bm;
     b.q0 = L.q0;
     b.q1 = L.q1;
     b.light = L.light;
-    b.heavy = L.heavy;
-    b.heavy_cb = L.heavy_cb;
-    b.chunk_owner = L.chunk_owner;
+    b.chunks = L.chunks;
     b.samples = L.samples;
     b.ctrl = L.ctrl;
     for (int pol = 0; pol < 4; pol++)
-        for (int st = 0; st < 2; st++) {
-            int per_sm = 0;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kernel_for(pol, st), kBlock, 0);
-            if (e != cudaSuccess || per_sm < 1) {
-                delete h;
-                return e != cudaSuccess ? cuda_error(e, "occupancy query")
-                                        : set_error(SSSP_ERR_DEVICE, "round-loop kernel cannot be resident");
+        for (int st = 0; st < 2; st++)
+            for (int sn = 0; sn < 2; sn++) {
+                int per_sm = 0;
+                e = cudaFuncSetAttribute((const void*)kernel_for(pol, st, sn),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+                if (e == cudaSuccess)
+                    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kernel_for(pol, st, sn),
+                                                                      kBlock, kSmemBytes);
+                if (e != cudaSuccess || per_sm < 1) {
+                    delete h;
+                    return e != cudaSuccess ? cuda_error(e, "occupancy query")
+                                            : set_error(SSSP_ERR_DEVICE, "round-loop kernel cannot be resident");
+                }
+                h->grid[pol][st][sn] = per_sm * sms;
             }
-            h->grid[pol][st] = per_sm * sms;
-        }
     e = cudaMallocHost((void**)&h->h_ctrl, sizeof(Ctrl));
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev[0]);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev[1]);
@@ -658,6 +893,7 @@ sssp_status sssp_run_ex(sssp_handle* h, int32_t source, sssp_policy policy, uint
     memset(&o, 0, sizeof(o));
     if (opts) o = *opts;
     const bool st = (o.flags & SSSP_RUN_STATS) != 0;
+    const bool sn = (o.flags & SSSP_RUN_SNAPSHOT) != 0;
     RunParams p = h->base;
     p.dist = d_dist_out;
     p.source = source;
@@ -668,11 +904,11 @@ sssp_status sssp_run_ex(sssp_handle* h, int32_t source, sssp_policy policy, uint
     p.trace = st ? (sssp_round*)o.d_trace : nullptr;
     p.trace_cap = o.trace_cap;
     p.ext_count = o.d_ext_count;
-    KernelFn k = kernel_for(policy, st);
-    const int grid = h->grid[policy][st];
+    KernelFn k = kernel_for(policy, st, sn);
+    const int grid = h->grid[policy][st][sn];
     void* args[] = {&p};
     cudaEventRecord(h->ev[0], h->stream);
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kBlock), args, 0, h->stream);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kBlock), args, kSmemBytes, h->stream);
     if (e != cudaSuccess) return cuda_error(e, "round-loop launch");
     cudaEventRecord(h->ev[1], h->stream);
     e = cudaMemcpyAsync(&h->h_ctrl->status, &h->ctrl->status, sizeof(Ctrl) - offsetof(Ctrl, status),

@@ -1,0 +1,8 @@
+set -x
+./scripts/bench_barrier > gpurun_out/bench_barrier.log 2>&1; echo "barrier rc=$?"; cat gpurun_out/bench_barrier.log
+timeout 900 python -m pytest tests -m "gpu and not slow" -x -q > gpurun_out/gpu_tests5.log 2>&1; echo "tests rc=$?"
+tail -3 gpurun_out/gpu_tests5.log
+for lib in libsssp.so libsssp_mb1.so; do
+  SSSP_LIB=$PWD/paper_2105_06145_b200/$lib timeout 900 python scripts/sweep.py --reps 3 --configs rmat24,grid4096,rgg4m --only rho:262144,rho:4096,bellman_ford:0 --out gpurun_out/sweep_r1d.jsonl --trace gpurun_out/trace_r1d.jsonl > gpurun_out/sweep_r1d_$lib.log 2>&1; echo "sweep $lib rc=$?"
+  cat gpurun_out/sweep_r1d_$lib.log
+done

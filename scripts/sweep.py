@@ -36,6 +36,9 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out", default=None)
     ap.add_argument("--only", default=None, help="policy:param,... overrides the built-in sweep")
+    ap.add_argument("--snapshot", action="store_true", help="deterministic (snapshot) rounds")
+    ap.add_argument("--trace", default=None, help="append per-round traces of the stats runs here (jsonl)")
+    ap.add_argument("--tag", default=os.environ.get("SSSP_LIB", "default"))
     args = ap.parse_args()
     import torch
 
@@ -55,18 +58,25 @@ def main():
             cases = [(c.split(":")[0], int(c.split(":")[1])) for c in args.only.split(",")]
         print(f"== {name}: n={g.n} m={g.m} src={g.source} gen {tg:.1f}s", flush=True)
         for pol, par in cases:
+            snap = args.snapshot
             for _ in range(2):
-                h.run(g.source, pol, par, out=d)
+                h.run(g.source, pol, par, out=d, snapshot=snap)
             ks, rs = [], []
             for r in range(args.reps):
                 flush.zero_()
-                h.run(g.source, pol, par, out=d, seed=r)
+                h.run(g.source, pol, par, out=d, seed=r, snapshot=snap)
                 ks.append(h.last_stats["kernel_ms"])
                 rs.append(h.last_stats["rounds"])
-            _, st, _, _ = h.run(g.source, pol, par, out=d, stats=True)
+            _, st, tr, _ = h.run(g.source, pol, par, out=d, stats=True, trace_cap=1 << 20 if args.trace else 0,
+                                 snapshot=snap)
+            if args.trace and tr is not None:
+                with open(args.trace, "a") as f:
+                    f.write(json.dumps({"config": name, "policy": pol, "param": par, "tag": args.tag,
+                                        "snapshot": snap, "rounds": {k: tr[k].tolist() for k in tr.dtype.names}})
+                            + "\n")
             km = statistics.median(ks)
             bt = 8 * st["queue_scanned"] + 8 * st["extracted"] + 16 * st["edges"]
-            rec = {"config": name, "policy": pol, "param": par, "kernel_ms": km, "kernel_ms_min": min(ks),
+            rec = {"config": name, "policy": pol, "param": par, "tag": args.tag, "snapshot": snap, "kernel_ms": km, "kernel_ms_min": min(ks),
                    "gteps": g.m / km / 1e6, "rounds": statistics.median(rs), "stats_rounds": st["rounds"],
                    "bytes_touched": bt, "touched_gbs": bt / km / 1e6, "frac_6552": bt / km / 1e6 / 6552.6,
                    "edges_per_m": st["edges"] / g.m, "qscan_per_n": st["queue_scanned"] / g.n,

@@ -36,7 +36,11 @@ def test_full_config(cuda_device, name):
             bad = np.flatnonzero(got != want)
             raise AssertionError(f"{name}/{pol}/{par}: {len(bad)} mismatches, first {bad[0]}: "
                                  f"{got[bad[0]]} vs {want[bad[0]]}")
-        assert h.last_stats["rounds"] >= kn + 1  # snapshot semantics lower bound
+    assert oracle.certify(g, got) == 0
+    # snapshot semantics: BF makes exactly k_n + 1 rounds, every policy at least k_n + 1
+    for pol, par in CASES[name][:1] + [("bellman_ford", 0)]:
+        got = P.dist_to_u64(h.run(g.source, pol, par, snapshot=True))
+        assert np.array_equal(got, want), f"{name}/{pol}/{par}/snapshot"
+        assert h.last_stats["rounds"] >= kn + 1
         if pol == "bellman_ford":
             assert h.last_stats["rounds"] == kn + 1
-    assert oracle.certify(g, got) == 0

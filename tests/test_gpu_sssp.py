@@ -48,9 +48,10 @@ def test_golden_examples(cuda_device):
         want = np.array(golden_value(c["dist"]), dtype=np.uint64)
         h = P.SSSP.from_graph(g, validate=True)
         for pol, par in SMALL_POLICIES:
-            _assert_same(_run(h, g, pol, par), want, f"{c['name']}/{pol}/{par}")
+            for snap in (False, True):
+                _assert_same(_run(h, g, pol, par, snapshot=snap), want, f"{c['name']}/{pol}/{par}/snap{snap}")
         if "bf_rounds" in c:
-            _, st, tr, _ = h.run(g.source, "bellman_ford", 0, trace_cap=64)
+            _, st, tr, _ = h.run(g.source, "bellman_ford", 0, trace_cap=64, snapshot=True)
             assert st["rounds"] == c["bf_rounds"]
             assert tr["fsize"].tolist() == c["bf_visited_per_round"]
 
@@ -62,11 +63,13 @@ def test_configs_small_all_policies(cuda_device, name):
     want = oracle.dijkstra(g)
     h = P.SSSP.from_graph(g, validate=True)
     for pol, par in SMALL_POLICIES + [("rho", 1 << 10), ("rho", 1 << 15)]:
-        got = _run(h, g, pol, par)
-        _assert_same(got, want, f"{name}/{pol}/{par}")
+        for snap in (False, True):
+            got = _run(h, g, pol, par, snapshot=snap)
+            _assert_same(got, want, f"{name}/{pol}/{par}/snap{snap}")
     for pol, par in (("rho", 256), ("rho", 4096)):
         _assert_same(_run(h, g, pol, par, exact=True), want, f"{name}/{pol}/{par}/exact")
         _assert_same(_run(h, g, pol, par, warmup=False), want, f"{name}/{pol}/{par}/nowarm")
+        _assert_same(_run(h, g, pol, par, exact=True, snapshot=True), want, f"{name}/{pol}/{par}/exact/snap")
 
 
 def test_random_graphs(cuda_device):
@@ -75,7 +78,8 @@ def test_random_graphs(cuda_device):
         want = oracle.dijkstra(g)
         h = P.SSSP.from_graph(g)
         for pol, par in (("rho", 2), ("rho", 100), ("delta", 1000), ("bellman_ford", 0), ("dijkstra", 0)):
-            _assert_same(_run(h, g, pol, par), want, f"{g.name}/src{g.source}/{pol}/{par}")
+            for snap in (False, True):
+                _assert_same(_run(h, g, pol, par, snapshot=snap), want, f"{g.name}/src{g.source}/{pol}/{par}/{snap}")
 
 
 def test_edge_cases(cuda_device):
@@ -113,7 +117,8 @@ def test_edge_cases(cuda_device):
     want = oracle.dijkstra(g)
     h = P.SSSP.from_graph(g)
     for pol, par in SMALL_POLICIES:
-        _assert_same(_run(h, g, pol, par), want, f"hub/{pol}/{par}")
+        for snap in (False, True):
+            _assert_same(_run(h, g, pol, par, snapshot=snap), want, f"hub/{pol}/{par}/snap{snap}")
 
 
 def test_errors(cuda_device):
@@ -166,7 +171,7 @@ def test_round_trace_parity(cuda_device, name):
              ("rho", 64, dict(exact=True, warmup=False)), ("rho", 2048, dict(exact=True, warmup=False)),
              ("rho", 512, dict(exact=True, warmup=True))]
     for pol, par, kw in cases:
-        d, st, tr, ext = h.run(g.source, pol, par, trace_cap=1 << 16, ext_counts=True, **kw)
+        d, st, tr, ext = h.run(g.source, pol, par, trace_cap=1 << 16, ext_counts=True, snapshot=True, **kw)
         d = P.dist_to_u64(d)
         _assert_same(d, d_ref, f"{name}/{pol}/{par}")
         _, tr_ref, ext_ref = oracle.stepping_sim(g, pol, par, exact=kw.get("exact", True),
@@ -183,7 +188,8 @@ def test_round_trace_parity(cuda_device, name):
 
 
 def test_sampled_rho_invariants(cuda_device):
-    """Sampled theta depends on queue order, so only invariants are compared."""
+    """Sampled theta depends on queue order, so only invariants are compared (snapshot
+    semantics for the round bounds; live rounds only keep the queue identities)."""
     P = _P()
     g = gen.make("rmat12")
     d_ref, hops = oracle.dijkstra(g, with_hops=True)
@@ -192,6 +198,11 @@ def test_sampled_rho_invariants(cuda_device):
     for rho in (16, 256, 4096):
         for seed in range(3):
             d, st, tr, ext = h.run(g.source, "rho", rho, seed=seed, trace_cap=4096, ext_counts=True)
+            _assert_same(P.dist_to_u64(d), d_ref, f"rho{rho}/seed{seed}/live")
+            q = tr["qsize"]
+            assert (q[1:] == q[:-1] - tr["fsize"][:-1] + tr["inserts"][:-1]).all()
+            assert q[-1] - tr["fsize"][-1] + tr["inserts"][-1] == 0
+            d, st, tr, ext = h.run(g.source, "rho", rho, seed=seed, trace_cap=4096, ext_counts=True, snapshot=True)
             _assert_same(P.dist_to_u64(d), d_ref, f"rho{rho}/seed{seed}")
             assert st["rounds"] >= kn + 1
             reach = hops >= 0
