@@ -1,9 +1,9 @@
 // run.cu — the stepping-algorithm round loop (Alg. 1) as ONE persistent
 // cooperative kernel, plus the sssp_* handle API.
 //
-// LaB-PQ of the round loop (DESIGN.md §5 "Queue state"): the membership flag of a
-// vertex lives in the top bit of its delta word (bit 63 set = NOT in Q), the value
-// in the low 63 bits; the queue is a compacted id array (ping-pong per round).
+// LaB-PQ of the round loop: the membership flag of a vertex lives in
+// the top bit of its delta word (bit 63 set = NOT in Q), the value in the low 63
+// bits; the queue is a compacted id array (ping-pong per round).
 //   Update(v)   = the WriteMin CAS that lowers the value also clears bit 63; the
 //                 thread whose CAS saw bit 63 set appends v (exactly one append per
 //                 insertion, no duplicates).
@@ -12,19 +12,26 @@
 // Because flag and key share one word, a concurrent WriteMin and Extract can never
 // lose an update, so Extract and relax may overlap ("live" rounds, the default).
 //
+// Append lists (next queue, heavy-chunk descriptors) are SHARDED: kShards segments,
+// each with its own counter on its own L2 slice, plus a spill segment.  Same-address
+// atomics serialise in the L2 (~7 ns each), so one shared tail counter capped the
+// queue scan at ~0.5 TB/s; warps stage appends in shared memory and reserve space in
+// their shard once per <= 256 ids.  Readers see a list as the concatenation of its
+// segments (prefix of the segment counts, computed per CTA in shared memory).
+//
 // Per round r:
 //   ExtDist  theta_r per policy (Table tab:framework).  rho: every CTA
-//            draws the same counter-based samples into shared memory and radix-
-//            selects the same theta (readings R5/R6) -> no barrier.
+//            draws the same counter-based samples into shared memory and selects
+//            the same theta (readings R5/R6) -> no barrier.
 //   Phase A  one pass over the queue (array LaB-PQ P:1011-1012): ids with
-//            key <= theta are extracted; vertices of degree <= kLight are relaxed at
-//            once by the extracting warp (live) or listed (snapshot mode); heavier
-//            ones are cut into kChunk-arc descriptors; the rest of Q is compacted
-//            into the next queue.                                     grid barrier
+//            key <= theta are extracted; vertices of degree <= kLight are relaxed by
+//            the extracting warp (live) or listed (snapshot mode); heavier ones are
+//            cut into kChunk-arc descriptors; the rest of Q is compacted into the
+//            next queue.                                              grid barrier
 //   Phase B  warps stride over the chunk descriptors (and, in snapshot mode, the
-//            light list): per arc c = d_u + w, plain L2 load filter, WriteMin by
-//            CAS, append on insertion.       grid barrier (only if non-empty)
-//   loop while |Q| > 0: |Q_{r+1}| is the next queue's tail counter.
+//            light list): per arc c = d_u + w, plain L2 load filter, WriteMin by CAS
+//            (P:697), append on insertion.          grid barrier (only if non-empty)
+//   loop while |Q| > 0.
 #include <stdio.h>
 
 #include <algorithm>
@@ -35,10 +42,11 @@
 
 namespace sssp {
 
-constexpr uint64_t kTop = 1ull << 63;  // flag bit: set = not in Q
-constexpr uint64_t kVal = kTop - 1;    // value bits of a delta word
 #ifndef SSSP_MIN_BLOCKS
-#define SSSP_MIN_BLOCKS 2
+#define SSSP_MIN_BLOCKS 1
+#endif
+#ifndef SSSP_BLOCK
+#define SSSP_BLOCK 768
 #endif
 #ifndef SSSP_ARCS
 #define SSSP_ARCS 8
@@ -46,13 +54,25 @@ constexpr uint64_t kVal = kTop - 1;    // value bits of a delta word
 #ifndef SSSP_LIGHT
 #define SSSP_LIGHT 128
 #endif
-constexpr int kBlock = 512;                 // threads per CTA of the round loop
-constexpr int kMinBlocks = SSSP_MIN_BLOCKS; // CTAs per SM the register budget targets
-constexpr int kArcs = SSSP_ARCS;            // arcs per lane in flight
-constexpr int kChunk = 32 * kArcs;     // arcs per heavy-chunk descriptor
-constexpr int kLight = SSSP_LIGHT;     // out-degree <= kLight: relaxed by the extracting warp
-constexpr int kSmemSamples = 4096;     // theta samples held in shared memory (else CTA-0 fallback)
-constexpr int kRankSelect = 256;       // s <= this: select by rank counting
+constexpr uint64_t kTop = 1ull << 63;        // flag bit: set = not in Q
+constexpr uint64_t kVal = kTop - 1;          // value bits of a delta word
+constexpr int kBlock = SSSP_BLOCK;           // threads per CTA of the round loop
+constexpr int kMinBlocks = SSSP_MIN_BLOCKS;  // CTAs per SM the register budget targets
+constexpr int kArcs = SSSP_ARCS;             // arcs per lane in flight
+constexpr int kChunk = 32 * kArcs;           // arcs per heavy-chunk descriptor
+constexpr int kLight = SSSP_LIGHT;           // out-degree <= kLight: relaxed by the extracting warp
+constexpr int kSmemSamples = 4096;           // theta samples held in shared memory (else CTA-0 fallback)
+constexpr int kRankSelect = 256;             // s <= this: select by rank counting
+constexpr int kWarps = kBlock / 32;
+constexpr int kEnt = 4;                      // queue entries per lane per Extract step
+constexpr int kQBuf = 256;                   // staged queue ids per warp (>= 32 * kArcs)
+constexpr int kLBuf = 32 * kEnt + 32;        // staged light vertices per warp
+constexpr int kShards = 32;                  // append-list segments (+1 spill)
+constexpr int kSeg = kShards + 1;
+constexpr int kCntStride = 256;              // int32 words between counters (1 KB: distinct L2 slices)
+constexpr int kMaxCtas = 4096;
+static_assert(32 * kArcs <= kQBuf, "one relax step must fit the stage");
+static_assert(kBlock % 32 == 0 && kBlock <= 1024, "block size");
 
 // A vertex (or a piece of one) to relax: snapshot key and a CSR arc range.
 struct __align__(16) Desc {
@@ -61,30 +81,39 @@ struct __align__(16) Desc {
     int32_t len;
 };
 
+// Per-round control (triple-buffered by round slot).
 struct __align__(128) RoundCnt {
-    int32_t tail;    // next-queue write cursor (remaining ids, then inserted ids)
-    int32_t nlight;  // snapshot mode: light frontier entries
-    int32_t nchunk;  // heavy chunk descriptors
-    int32_t nheavy;  // STATS: heavy vertices
-    unsigned long long minrem;   // min key among ids Extract kept in Q
-    unsigned long long minsucc;  // min successful WriteMin value
+    int32_t nlight;              // snapshot mode: light frontier entries
+    int32_t nheavy;              // STATS: heavy vertices
     unsigned long long theta;    // CTA-0 fallback theta
     unsigned long long fsize;    // STATS: extracted
     unsigned long long edges;    // STATS: arcs of extracted vertices
     unsigned long long succ;     // STATS: successful WriteMins
     unsigned long long inserts;  // STATS: ids appended by relax
-    unsigned long long pad[5];
+    unsigned long long pad[10];
 };
 
 struct __align__(128) Ctrl {
-    unsigned bar;  // grid barrier arrival counter
-    unsigned pad0[31];
     RoundCnt cnt[3];
     // results (copied to the host after the run)
     int32_t status;
     int32_t pad1;
     int64_t rounds;
     int64_t tot_extracted, tot_edges, tot_succ, tot_inserts, tot_qscan, max_q, max_f;
+};
+
+// A sharded append list: segment s < kShards holds [s*cap, s*cap + min(count_s, cap)),
+// the spill segment [kShards*cap, ...).  Counters live 1 KB apart.
+template <typename T>
+struct Sharded {
+    T* base;
+    int32_t* cnt;  // cnt[s * kCntStride]
+    int64_t cap;   // per-shard capacity
+    __device__ __forceinline__ T* seg(int s) const { return base + (int64_t)s * cap; }
+    __device__ __forceinline__ int64_t seg_count(int s) const {
+        const int64_t c = __ldcg(cnt + s * kCntStride);
+        return s < kShards ? (c < cap ? c : cap) : c;
+    }
 };
 
 struct RunParams {
@@ -95,10 +124,13 @@ struct RunParams {
     const int32_t* __restrict__ idx;
     const uint32_t* __restrict__ w;
     uint64_t* dist;
-    int32_t* q0;
-    int32_t* q1;
+    int32_t* qbuf[2];   // queue storage, ping-pong
+    int64_t qcap;       // per-shard queue capacity
+    Desc* chunks;       // chunk descriptor storage
+    int64_t ccap;       // per-shard chunk capacity
+    int32_t* counters;  // [3 slots][2 lists: queue, chunks][kSeg] * kCntStride
+    uint64_t* cta_min;  // [3 slots][kMaxCtas]: per-CTA min for Delta / Dijkstra
     Desc* light;
-    Desc* chunks;
     uint64_t* samples;
     Ctrl* ctrl;
     uint64_t param;
@@ -110,13 +142,20 @@ struct RunParams {
     int32_t* ext_count;
 };
 
+__device__ __forceinline__ int32_t* counters_of(const RunParams& p, int slot, int list) {
+    return p.counters + (int64_t)((slot * 2 + list) * kSeg) * kCntStride;
+}
+__device__ __forceinline__ Sharded<int32_t> queue_of(const RunParams& p, int64_t round_of_queue) {
+    // Q_r lives in qbuf[r & 1]; its counts are in slot (r + 2) % 3
+    return Sharded<int32_t>{p.qbuf[round_of_queue & 1], counters_of(p, (int)((round_of_queue + 2) % 3), 0), p.qcap};
+}
+__device__ __forceinline__ Sharded<Desc> chunks_of(const RunParams& p, int64_t r) {
+    return Sharded<Desc>{p.chunks, counters_of(p, (int)(r % 3), 1), p.ccap};
+}
+
 __device__ __forceinline__ void reset_cnt(RoundCnt* c) {
-    c->tail = 0;
     c->nlight = 0;
-    c->nchunk = 0;
     c->nheavy = 0;
-    c->minrem = kInf;
-    c->minsucc = kInf;
     c->theta = 0;
     c->fsize = 0;
     c->edges = 0;
@@ -152,16 +191,42 @@ __device__ __forceinline__ int64_t warp_rank() { return (int64_t)(threadIdx.x >>
 
 __host__ __device__ constexpr bool uses_min(int pol) { return pol == SSSP_DELTA || pol == SSSP_DIJKSTRA; }
 
-// --------------------------------------------------------------------- per-warp staging
-// Appends to the next queue, and light vertices waiting to be relaxed, are staged in a
-// warp-private shared-memory buffer: one global atomicAdd per ~kQBuf appended ids
-// instead of one per warp step, and the flush is a coalesced store.
-constexpr int kWarps = kBlock / 32;
-constexpr int kEnt = 4;     // queue entries per lane per Extract step
-constexpr int kQBuf = 256;  // staged queue ids per warp (>= 32 * kArcs)
-constexpr int kLBuf = 32 * kEnt + 32;  // staged light vertices per warp
-static_assert(32 * kArcs <= kQBuf, "one relax step must fit the stage");
+// --------------------------------------------------------------------- segment prefix
+// Exclusive prefix of a sharded list's segment counts, in shared memory (pref[kSeg] =
+// total).  Called by all threads; ends with __syncthreads.
+template <typename T>
+__device__ __forceinline__ void load_prefix(const Sharded<T>& L, int64_t* pref) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const int64_t c0 = L.seg_count(lane);                     // shards 0..31
+        const int64_t c1 = lane == 0 ? L.seg_count(kShards) : 0;  // spill
+        int64_t x = c0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t t = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += t;
+        }
+        const int64_t spill = __shfl_sync(kFull, c1, 0);
+        pref[lane] = x - c0;
+        if (lane == 31) {
+            pref[kShards] = x;
+            pref[kSeg] = x + spill;
+        }
+    }
+    __syncthreads();
+}
+static_assert(kShards == 32, "load_prefix assumes one warp of shards");
 
+// segment of virtual index i < total: largest s with pref[s] <= i (pref is smem)
+__device__ __forceinline__ int seg_of(const int64_t* pref, int64_t i) {
+    int s = 0;
+#pragma unroll
+    for (int step = 32; step > 0; step >>= 1)
+        if (s + step <= kShards && pref[s + step] <= i) s += step;
+    return s;
+}
+
+// --------------------------------------------------------------------- per-warp staging
 struct WarpStage {
     Desc light[kLBuf];
     int32_t q[kQBuf];
@@ -175,20 +240,44 @@ struct Acc {
 
 struct Warp {  // per-warp working state (qn, ln are warp-uniform)
     WarpStage* st;
-    int32_t* qnext;
+    Sharded<int32_t> qnext;
     RoundCnt* C;
+    int shard;
     int32_t qn;
     int32_t ln;
     Acc acc;
 };
 
+// Reserve `tot` slots of a sharded list for this warp (lane 0 does the atomics).
+// Element i < tot goes to p0 + i if i < fit, else to p1 + (i - fit) (spill segment).
+template <typename T>
+__device__ __forceinline__ void reserve(const Sharded<T>& L, int shard, int32_t tot, T*& p0, int32_t& fit, T*& p1) {
+    int64_t pos = 0, spos = 0;
+    if (lane_id() == 0) {
+        pos = atomicAdd(L.cnt + shard * kCntStride, tot);
+        const int64_t f = pos >= L.cap ? 0 : (L.cap - pos < tot ? L.cap - pos : tot);
+        if (f < tot) spos = atomicAdd(L.cnt + kShards * kCntStride, (int32_t)(tot - f));
+    }
+    pos = __shfl_sync(kFull, pos, 0);
+    spos = __shfl_sync(kFull, spos, 0);
+    fit = pos >= L.cap ? 0 : (int32_t)(L.cap - pos < tot ? L.cap - pos : tot);
+    p0 = L.seg(shard) + pos;
+    p1 = L.seg(kShards) + spos;
+}
+
 __device__ __forceinline__ void wq_flush(Warp& W) {
     if (W.qn == 0) return;
     __syncwarp();
-    int32_t base = 0;
-    if (lane_id() == 0) base = atomicAdd(&W.C->tail, W.qn);
-    base = __shfl_sync(kFull, base, 0);
-    for (int32_t i = lane_id(); i < W.qn; i += 32) W.qnext[base + i] = W.st->q[i];
+    int32_t *p0, *p1;
+    int32_t fit;
+    reserve(W.qnext, W.shard, W.qn, p0, fit, p1);
+    for (int32_t i = lane_id(); i < W.qn; i += 32) {
+        const int32_t v = W.st->q[i];
+        if (i < fit)
+            p0[i] = v;
+        else
+            p1[i - fit] = v;
+    }
     __syncwarp();
     W.qn = 0;
 }
@@ -228,11 +317,30 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
     uint64_t cur[kArcs];
 #pragma unroll
     for (int t = 0; t < kArcs; t++) cur[t] = v[t] >= 0 ? ld_cg_u64(p.dist + v[t]) : 0ull;
+    // first CAS attempt of every slot issued back to back (one round trip, not kArcs),
+    // then the rare retries
+    uint64_t old[kArcs];
+#pragma unroll
+    for (int t = 0; t < kArcs; t++)
+        old[t] = (v[t] >= 0 && (cur[t] & kVal) > c[t])
+                     ? atomicCAS((unsigned long long*)(p.dist + v[t]), (unsigned long long)cur[t],
+                                 (unsigned long long)c[t])
+                     : cur[t] + 1;  // "no attempt" marker: != cur[t]
     int32_t cnt = 0;
     bool app[kArcs];
 #pragma unroll
     for (int t = 0; t < kArcs; t++) {
-        app[t] = v[t] >= 0 && write_min<POL, STATS>(p.dist, v[t], c[t], cur[t], W.acc);
+        if (v[t] >= 0 && (cur[t] & kVal) > c[t]) {
+            if (old[t] == cur[t]) {
+                if (STATS) W.acc.succ++;
+                if (uses_min(POL)) W.acc.minsucc = c[t] < W.acc.minsucc ? c[t] : W.acc.minsucc;
+                app[t] = (cur[t] & kTop) != 0;
+            } else {
+                app[t] = write_min<POL, STATS>(p.dist, v[t], c[t], old[t], W.acc);
+            }
+        } else {
+            app[t] = false;
+        }
         cnt += app[t];
     }
     if (!__any_sync(kFull, cnt != 0)) return;
@@ -339,9 +447,9 @@ __device__ __forceinline__ void light_drain(const RunParams& p, Warp& W) {
     relax_vertices<POL, STATS>(p, e.d, e.beg, e.len, W);
 }
 
-// Cut the heavy lanes' vertices into kChunk-arc descriptors; one atomic per warp.
-__device__ __forceinline__ void emit_chunks(const RunParams& p, bool heavy, uint64_t d, int32_t beg, int32_t deg,
-                                            RoundCnt* C, bool stats) {
+// Cut the heavy lanes' vertices into kChunk-arc descriptors (one reservation per warp).
+__device__ __forceinline__ void emit_chunks(const Sharded<Desc>& CL, int shard, bool heavy, uint64_t d, int32_t beg,
+                                            int32_t deg, RoundCnt* C, bool stats) {
     const uint32_t hm = __ballot_sync(kFull, heavy);
     if (!hm) return;
     const int lane = lane_id();
@@ -349,12 +457,10 @@ __device__ __forceinline__ void emit_chunks(const RunParams& p, bool heavy, uint
     const int32_t incl = warp_incl_scan(nch);
     const int32_t tot = __shfl_sync(kFull, incl, 31);
     const int32_t excl = incl - nch;
-    int32_t base = 0;
-    if (lane == 0) {
-        base = atomicAdd(&C->nchunk, tot);
-        if (stats) atomicAdd(&C->nheavy, __popc(hm));
-    }
-    base = __shfl_sync(kFull, base, 0);
+    if (stats && lane == 0) atomicAdd(&C->nheavy, __popc(hm));
+    Desc *p0, *p1;
+    int32_t fit;
+    reserve(CL, shard, tot, p0, fit, p1);
     for (int32_t j0 = 0; j0 < tot; j0 += 32) {
         const int32_t j = j0 + lane;
         int32_t o = 0;
@@ -369,7 +475,7 @@ __device__ __forceinline__ void emit_chunks(const RunParams& p, bool heavy, uint
         const uint64_t odd = __shfl_sync(kFull, d, o);
         if (j < tot) {
             const int32_t k = (j - oe) * kChunk;
-            st_desc(p.chunks + base + j, odd, ob + k, min(kChunk, od - k));
+            st_desc(j < fit ? p0 + j : p1 + (j - fit), odd, ob + k, min(kChunk, od - k));
         }
     }
 }
@@ -377,22 +483,29 @@ __device__ __forceinline__ void emit_chunks(const RunParams& p, bool heavy, uint
 // --------------------------------------------------------------------- phase A
 // Extract(theta): kEnt queue entries per lane per step, all loads issued together.
 template <int POL, bool STATS, bool SNAP>
-__device__ __forceinline__ void phase_a(const RunParams& p, const int32_t* __restrict__ qcur, int32_t q,
-                                        uint64_t theta, Warp& W) {
+__device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_t>& QC, const int64_t* qpref,
+                                        const Sharded<Desc>& CL, uint64_t theta, uint64_t& minrem, Warp& W) {
     const int lane = lane_id();
+    const int64_t q = qpref[kSeg];
     const int64_t gw = warp_rank();
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    uint64_t minrem = kInf, fs = 0, edges = 0;
+    uint64_t fs = 0, edges = 0;
     // kEnt entries per lane only when every warp gets at least two such steps; small
     // queues are spread one entry per lane so that more warps share the round
-    const int ent = (int64_t)q >= nwarps * (64 * kEnt) ? kEnt : 1;
+    const int ent = q >= nwarps * (64 * kEnt) ? kEnt : 1;
     for (int64_t base = gw * (32 * ent); base < q; base += nwarps * (32 * ent)) {
         int32_t id[kEnt];
         uint64_t val[kEnt];
+        const int sg = seg_of(qpref, base);  // warp-uniform
 #pragma unroll
         for (int e = 0; e < kEnt; e++) {
             const int64_t i = base + e * 32 + lane;
-            id[e] = (e < ent && i < q) ? ld_cg_i32(qcur + i) : -1;
+            id[e] = -1;
+            if (e < ent && i < q) {
+                int s = sg;
+                while (qpref[s + 1] <= i) s++;
+                id[e] = ld_cg_i32(QC.seg(s) + (i - qpref[s]));
+            }
         }
 #pragma unroll
         for (int e = 0; e < kEnt; e++) val[e] = id[e] >= 0 ? (ld_cg_u64(p.dist + id[e]) & kVal) : kVal;
@@ -423,7 +536,7 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const int32_t* __res
             }
             const bool heavy = take && deg[e] > kLight;
             const bool light = take && deg[e] > 0 && !heavy;
-            emit_chunks(p, heavy, val[e], beg[e], deg[e], W.C, STATS);
+            emit_chunks(CL, W.shard, heavy, val[e], beg[e], deg[e], W.C, STATS);
             if (SNAP) {
                 const int32_t ls = warp_append_slot(light, &W.C->nlight);
                 if (light) st_desc(p.light + ls, val[e], beg[e], deg[e]);
@@ -434,10 +547,6 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const int32_t* __res
         if (!SNAP) light_relax_full<POL, STATS>(p, W);
     }
     if (!SNAP) light_drain<POL, STATS>(p, W);
-    if (uses_min(POL)) {
-        minrem = warp_min_u64(minrem);
-        if (lane == 0 && minrem != kInf) atomicMin(&W.C->minrem, (unsigned long long)minrem);
-    }
     if (STATS) {
         fs = warp_sum(fs);
         edges = warp_sum(edges);
@@ -448,15 +557,21 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const int32_t* __res
 
 // --------------------------------------------------------------------- phase B
 template <int POL, bool STATS, bool SNAP>
-__device__ __forceinline__ void phase_b(const RunParams& p, int32_t nl, int32_t nc, Warp& W) {
+__device__ __forceinline__ void phase_b(const RunParams& p, const Sharded<Desc>& CL, const int64_t* cpref, int32_t nl,
+                                        Warp& W) {
     const int lane = lane_id();
     const int64_t gw = warp_rank();
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nb = SNAP ? ((int64_t)nl + 31) / 32 : 0;
+    const int64_t nc = cpref[kSeg];
     const int64_t total = nb + nc;
+    auto chunk_at = [&](int64_t i) {  // i-th descriptor of the concatenated segments
+        const int s = seg_of(cpref, i);
+        return ld_desc(CL.seg(s) + (i - cpref[s]));
+    };
     int64_t item = gw;
     Desc nxt;
-    if (item >= nb && item < total) nxt = ld_desc(p.chunks + (item - nb));
+    if (item >= nb && item < total) nxt = chunk_at(item - nb);
     for (; item < total; item += nwarps) {
         if (SNAP && item < nb) {
             const int64_t j = item * 32 + lane;
@@ -469,10 +584,10 @@ __device__ __forceinline__ void phase_b(const RunParams& p, int32_t nl, int32_t 
                 e.len = 0;
             }
             relax_vertices<POL, STATS>(p, e.d, e.beg, e.len, W);
-            if (item + nwarps >= nb && item + nwarps < total) nxt = ld_desc(p.chunks + (item + nwarps - nb));
+            if (item + nwarps >= nb && item + nwarps < total) nxt = chunk_at(item + nwarps - nb);
         } else {
             const Desc e = nxt;
-            if (item + nwarps < total) nxt = ld_desc(p.chunks + (item + nwarps - nb));  // prefetch
+            if (item + nwarps < total) nxt = chunk_at(item + nwarps - nb);  // prefetch
             relax_chunk<POL, STATS>(p, e.d, e.beg, e.len, W);
         }
     }
@@ -481,16 +596,13 @@ __device__ __forceinline__ void phase_b(const RunParams& p, int32_t nl, int32_t 
 template <int POL, bool STATS>
 __device__ __forceinline__ void flush_acc(Warp& W) {
     wq_flush(W);
-    if (uses_min(POL)) {
-        const uint64_t mn = warp_min_u64(W.acc.minsucc);
-        if (lane_id() == 0 && mn != kInf) atomicMin(&W.C->minsucc, (unsigned long long)mn);
-    }
     if (STATS) {
         const uint32_t s = warp_sum(W.acc.succ), ins = warp_sum(W.acc.inserts);
         if (lane_id() == 0 && s) atomicAdd(&W.C->succ, (unsigned long long)s);
         if (lane_id() == 0 && ins) atomicAdd(&W.C->inserts, (unsigned long long)ins);
     }
-    W.acc = Acc();
+    W.acc.succ = 0;
+    W.acc.inserts = 0;
 }
 
 // --------------------------------------------------------------------- ExtDist for rho
@@ -499,9 +611,13 @@ struct SmemKey {
     __device__ uint64_t operator()(int64_t i) const { return a[i]; }
 };
 struct QueueVal {  // value of the i-th queued id (flag bit masked off), read through L2
-    const int32_t* queue;
+    Sharded<int32_t> Q;
+    const int64_t* pref;
     const uint64_t* dist;
-    __device__ uint64_t operator()(int64_t i) const { return ld_cg_u64(dist + ld_cg_i32(queue + i)) & kVal; }
+    __device__ uint64_t operator()(int64_t i) const {
+        const int s = seg_of(pref, i);
+        return ld_cg_u64(dist + ld_cg_i32(Q.seg(s) + (i - pref[s]))) & kVal;
+    }
 };
 
 __device__ __forceinline__ uint64_t sample_index(uint64_t seed, int64_t round, uint64_t j, uint64_t q) {
@@ -515,7 +631,18 @@ __device__ __forceinline__ uint64_t cta_kth_by_rank(const uint64_t* keys, int s,
     if (tid < s) {
         const uint64_t x = keys[tid];
         uint32_t lt = 0, le = 0;
-        for (int j = 0; j < s; j++) {
+        int j = 0;
+        for (; j + 8 <= s; j += 8) {  // 8 independent broadcast loads in flight
+            uint64_t y[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) y[u] = keys[j + u];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                lt += y[u] < x;
+                le += y[u] <= x;
+            }
+        }
+        for (; j < s; j++) {
             const uint64_t y = keys[j];
             lt += y < x;
             le += y <= x;
@@ -532,41 +659,54 @@ __device__ __forceinline__ uint64_t cta_kth_by_rank(const uint64_t* keys, int s,
 template <int POL, bool STATS, bool SNAP>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    WarpStage* stage = (WarpStage*)smem_raw;                            // [kWarps]
-    uint64_t* s_keys = (uint64_t*)(smem_raw + kWarps * sizeof(WarpStage)); // [kSmemSamples]
+    WarpStage* stage = (WarpStage*)smem_raw;                                // [kWarps]
+    uint64_t* s_keys = (uint64_t*)(smem_raw + kWarps * sizeof(WarpStage));  // [kSmemSamples]
     SelectSmem& sm = *(SelectSmem*)(s_keys + kSmemSamples);
+    __shared__ int64_t qpref[kSeg + 1];  // segment prefix of Q_r
+    __shared__ int64_t cpref[kSeg + 1];  // segment prefix of the round's chunk list
+    __shared__ uint64_t bc_u[2];         // min_Q (Delta / Dijkstra), CTA-0 theta
+    __shared__ int32_t bc_nl;
+    __shared__ uint64_t red[kWarps];
     Ctrl* ctrl = p.ctrl;
     Warp W;
     W.st = stage + (threadIdx.x >> 5);
+    W.shard = (int)(warp_rank() % kShards);
     W.qn = 0;
     W.ln = 0;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
 
-    // Alg. 1 lines 1-2: delta[.] = +inf (not in Q), delta[s] = 0 (in Q), queue = {s}
+    // Alg. 1 lines 1-2: delta[.] = +inf (not in Q), delta[s] = 0 (in Q), Q_1 = {s}
     for (int64_t i = gtid; i < p.n; i += gsize) p.dist[i] = (i == p.source) ? 0ull : kInf;
     if (p.ext_count)
         for (int64_t i = gtid; i < p.n; i += gsize) p.ext_count[i] = 0;
+    for (int64_t i = gtid; i < 3 * 2 * kSeg; i += gsize) p.counters[i * kCntStride] = 0;
+    for (int64_t i = gtid; i < 3 * kMaxCtas; i += gsize) p.cta_min[i] = kInf;
     if (gtid == 0) {
-        p.q0[0] = p.source;
+        p.qbuf[1][0] = p.source;  // Q_1 lives in qbuf[1], shard 0
         for (int c = 0; c < 3; c++) reset_cnt(&ctrl->cnt[c]);
-        ctrl->cnt[0].tail = 1;    // |Q_1| = 1
-        ctrl->cnt[0].minrem = 0;  // min_Q delta = delta[s] = 0
         ctrl->status = 0;
         ctrl->rounds = 0;
         ctrl->tot_extracted = ctrl->tot_edges = ctrl->tot_succ = ctrl->tot_inserts = 0;
         ctrl->tot_qscan = ctrl->max_q = ctrl->max_f = 0;
     }
-    grid_sync(&ctrl->bar);
+    grid_sync(nullptr);
+    if (gtid == 0) {
+        p.counters[0] = 1;  // |Q_1| = 1 (slot 0, queue list, shard 0)
+        p.cta_min[0] = 0;   // min_Q delta = delta[s] = 0
+    }
+    grid_sync(nullptr);
 
     uint64_t theta_prev = 0;
     int warm = 0;
     int64_t r = 1;
     for (;; r++) {
-        RoundCnt* P = &ctrl->cnt[(r + 2) % 3];
         RoundCnt* C = &ctrl->cnt[r % 3];
-        const int32_t q = ld_volatile_i32(&P->tail);  // |Q_r|
-        if (q == 0) break;                             // while |Q| > 0
+        const Sharded<int32_t> QC = queue_of(p, r);
+        const Sharded<Desc> CL = chunks_of(p, r);
+        load_prefix(QC, qpref);
+        const int64_t q = qpref[kSeg];  // |Q_r|
+        if (q == 0) break;              // while |Q| > 0
         if (r > p.max_rounds) {
             if (gtid == 0) ctrl->status = SSSP_ERR_ROUNDS;
             break;
@@ -574,17 +714,30 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0;
         if (STATS && gtid == 0) t0 = globaltimer();
         if (gtid == 0) reset_cnt(&ctrl->cnt[(r + 1) % 3]);
-        const int32_t* qcur = (r & 1) ? p.q0 : p.q1;
-        int32_t* qnext = (r & 1) ? p.q1 : p.q0;
+        if (gtid < 2 * kSeg) {  // counters of slot (r+1)%3: written in round r+1, read in r+1 / r+2
+            p.counters[((int64_t)(((r + 1) % 3) * 2) * kSeg + gtid) * kCntStride] = 0;
+        }
+        W.qnext = queue_of(p, r + 1);
+        W.C = C;
 
         // ---- ExtDist (Table tab:framework)
         uint64_t theta;
         if (POL == SSSP_BELLMAN_FORD) {
             theta = kInf;
         } else if (POL == SSSP_DIJKSTRA || POL == SSSP_DELTA) {
-            const uint64_t a = ld_volatile_u64((const uint64_t*)&P->minrem);
-            const uint64_t b = ld_volatile_u64((const uint64_t*)&P->minsucc);
-            const uint64_t minq = a < b ? a : b;  // <= min_{v in Q} delta[v] (exact in snapshot mode)
+            // min_Q delta = min over the per-CTA minima of the previous round
+            if (threadIdx.x < 32) {
+                const uint64_t* cm = p.cta_min + ((r + 2) % 3) * kMaxCtas;
+                uint64_t mn = kInf;
+                for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) {
+                    const uint64_t x = __ldcg((const unsigned long long*)(cm + i));
+                    mn = x < mn ? x : mn;
+                }
+                mn = warp_min_u64(mn);
+                if (threadIdx.x == 0) bc_u[0] = mn;
+            }
+            __syncthreads();
+            const uint64_t minq = bc_u[0];  // <= min_{v in Q} delta[v] (exact in snapshot mode)
             if (POL == SSSP_DIJKSTRA) {
                 theta = minq;
             } else {
@@ -601,12 +754,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                 rho = rho / 10 ? rho / 10 : 1;  // reading R7
             }
             const uint64_t s = sample_count((uint64_t)q, rho);
+            const QueueVal qv{QC, qpref, p.dist};
             if ((uint64_t)q <= rho) {
                 theta = kInf;  // |Q| <= rho: extract all
             } else if (!(p.flags & SSSP_RUN_RHO_EXACT) && s <= (uint64_t)kSmemSamples) {
                 // every CTA draws the same samples and selects the same theta: no barrier
                 for (uint64_t j = threadIdx.x; j < s; j += blockDim.x)
-                    s_keys[j] = ld_cg_u64(p.dist + ld_cg_i32(qcur + sample_index(p.seed, r, j, (uint64_t)q))) & kVal;
+                    s_keys[j] = qv((int64_t)sample_index(p.seed, r, j, (uint64_t)q));
                 __syncthreads();
                 uint64_t k = (rho * s + (uint64_t)q - 1) / (uint64_t)q;
                 k = k < 1 ? 1 : (k > s ? s : k);
@@ -616,11 +770,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                 if (blockIdx.x == 0) {
                     uint64_t th;
                     if (p.flags & SSSP_RUN_RHO_EXACT) {
-                        th = cta_kth_smallest(QueueVal{qcur, p.dist}, q, rho, sm);
+                        th = cta_kth_smallest(qv, q, rho, sm);
                     } else {
                         for (uint64_t j = threadIdx.x; j < s; j += blockDim.x)
-                            p.samples[j] =
-                                ld_cg_u64(p.dist + ld_cg_i32(qcur + sample_index(p.seed, r, j, (uint64_t)q))) & kVal;
+                            p.samples[j] = qv((int64_t)sample_index(p.seed, r, j, (uint64_t)q));
                         __syncthreads();
                         uint64_t k = (rho * s + (uint64_t)q - 1) / (uint64_t)q;
                         k = k < 1 ? 1 : (k > s ? s : k);
@@ -628,26 +781,42 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                     }
                     if (threadIdx.x == 0) C->theta = th;
                 }
-                grid_sync(&ctrl->bar);
-                theta = ld_volatile_u64((const uint64_t*)&C->theta);
+                grid_sync(nullptr);
+                if (threadIdx.x == 0) bc_u[1] = __ldcg((const unsigned long long*)&C->theta);
+                __syncthreads();
+                theta = bc_u[1];
             }
         }
         if (STATS && gtid == 0) t1 = globaltimer();
 
         // ---- phase A: Extract(theta) (+ light relax in live mode)
-        W.qnext = qnext;
-        W.C = C;
-        phase_a<POL, STATS, SNAP>(p, qcur, q, theta, W);
+        uint64_t minrem = kInf;
+        phase_a<POL, STATS, SNAP>(p, QC, qpref, CL, theta, minrem, W);
         flush_acc<POL, STATS>(W);
-        grid_sync(&ctrl->bar);
+        grid_sync(nullptr);
         if (STATS && gtid == 0) t2 = globaltimer();
         // ---- phase B: heavy chunks (+ light list in snapshot mode)
-        const int32_t nc = ld_volatile_i32(&C->nchunk);
-        const int32_t nl = SNAP ? ld_volatile_i32(&C->nlight) : 0;
-        if (nc + nl > 0) {
-            phase_b<POL, STATS, SNAP>(p, nl, nc, W);
+        load_prefix(CL, cpref);
+        if (threadIdx.x == 0) bc_nl = SNAP ? __ldcg(&C->nlight) : 0;
+        __syncthreads();
+        const int32_t nl = bc_nl;
+        const bool phase_b_work = cpref[kSeg] + nl > 0;
+        if (phase_b_work) phase_b<POL, STATS, SNAP>(p, CL, cpref, nl, W);
+        if (uses_min(POL)) {  // this CTA's min over kept ids and successful WriteMins
+            uint64_t mn = warp_min_u64(minrem < W.acc.minsucc ? minrem : W.acc.minsucc);
+            if (lane_id() == 0) red[threadIdx.x >> 5] = mn;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int i = 1; i < kWarps; i++) mn = red[i] < mn ? red[i] : mn;
+                p.cta_min[(r % 3) * kMaxCtas + blockIdx.x] = mn;
+            }
+            W.acc.minsucc = kInf;
+        }
+        if (phase_b_work) {
             flush_acc<POL, STATS>(W);
-            grid_sync(&ctrl->bar);
+            grid_sync(nullptr);
+        } else if (uses_min(POL) || STATS) {
+            grid_sync(nullptr);
         }
         if (STATS && gtid == 0) t3 = globaltimer();
 
@@ -665,7 +834,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                 t->t_theta_ns = (int64_t)(t1 - t0);
                 t->t_extract_ns = (int64_t)(t2 - t1);
                 t->t_relax_ns = (int64_t)(t3 - t2);
-                t->reserved0 = C->nchunk;
+                t->reserved0 = cpref[kSeg];
                 t->reserved1 = 0;
             }
             ctrl->tot_extracted += f;
@@ -727,7 +896,12 @@ namespace {
 struct Layout {
     uint64_t* dist;
     int32_t *q0, *q1;
-    Desc *light, *chunks;
+    int64_t qcap;
+    Desc* chunks;
+    int64_t ccap;
+    int32_t* counters;
+    uint64_t* cta_min;
+    Desc* light;
     uint64_t* samples;
     Ctrl* ctrl;
     int32_t* err;
@@ -737,15 +911,22 @@ struct Layout {
 Layout carve(void* base, int32_t n, int64_t m) {
     Carver c(base);
     Layout L;
+    // queue: kShards segments of qcap (2x the even share + slack) plus a spill segment of n
+    L.qcap = 2 * (((int64_t)n + kShards - 1) / kShards) + 1024;
+    const int64_t qlen = kShards * L.qcap + n;
     // chunks per round <= sum over heavy extracted vertices of ceil(deg/kChunk)
-    const int64_t ccap = m / kChunk + std::min<int64_t>(n, m / (kLight + 1)) + 1;
+    const int64_t ctot = m / kChunk + std::min<int64_t>(n, m / (kLight + 1)) + 1;
+    L.ccap = 2 * ((ctot + kShards - 1) / kShards) + 256;
+    const int64_t clen = kShards * L.ccap + ctot;
     L.ctrl = c.take<Ctrl>(1);
     L.err = c.take<int32_t>(32);
+    L.counters = c.take<int32_t>((size_t)3 * 2 * kSeg * kCntStride);
+    L.cta_min = c.take<uint64_t>((size_t)3 * kMaxCtas);
     L.dist = c.take<uint64_t>(n);
-    L.q0 = c.take<int32_t>(n);
-    L.q1 = c.take<int32_t>(n);
+    L.q0 = c.take<int32_t>(qlen);
+    L.q1 = c.take<int32_t>(qlen);
+    L.chunks = c.take<Desc>(clen);
     L.light = c.take<Desc>(n);
-    L.chunks = c.take<Desc>(ccap);
     L.samples = c.take<uint64_t>(kMaxSamples);
     L.bytes = align_up(c.off, 256);
     return L;
@@ -824,10 +1005,14 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
     b.off = d_offsets;
     b.idx = d_indices;
     b.w = d_weights;
-    b.q0 = L.q0;
-    b.q1 = L.q1;
-    b.light = L.light;
+    b.qbuf[0] = L.q0;
+    b.qbuf[1] = L.q1;
+    b.qcap = L.qcap;
     b.chunks = L.chunks;
+    b.ccap = L.ccap;
+    b.counters = L.counters;
+    b.cta_min = L.cta_min;
+    b.light = L.light;
     b.samples = L.samples;
     b.ctrl = L.ctrl;
     for (int pol = 0; pol < 4; pol++)
@@ -844,7 +1029,7 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
                     return e != cudaSuccess ? cuda_error(e, "occupancy query")
                                             : set_error(SSSP_ERR_DEVICE, "round-loop kernel cannot be resident");
                 }
-                h->grid[pol][st][sn] = per_sm * sms;
+                h->grid[pol][st][sn] = std::min(per_sm * sms, kMaxCtas);
             }
     e = cudaMallocHost((void**)&h->h_ctrl, sizeof(Ctrl));
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev[0]);

@@ -55,8 +55,9 @@ def test_workspace_sizing_host_only():
     assert small > 0
     n, m = 1 << 24, 520_000_000
     big = P.sssp_workspace_bytes(n, m, 0)
-    # dist + 2 queues + light frontier: 8n + 8n + 16n; heavy list + chunk map: <= 28 m/65 + 4 m/256
-    assert 32 * n < big < 32 * n + 28 * (m // 65) + m // 64 + (64 << 20)
+    # dist 8n + two sharded queues (3n ids each) 24n + light frontier 16n = 48n; chunk
+    # descriptors: 3 x 16 B x (m/256 + m/129) (sharded at 2x + spill); counters/samples < 64 MiB
+    assert 48 * n < big < 48 * n + 48 * (m // 256 + m // 129 + 1) + (64 << 20)
     assert P.sssp_pq_workspace_bytes(1000) > 8 * 1000 // 8
 
 
