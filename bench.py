@@ -263,7 +263,7 @@ def main():
 
     # algorithmic bytes from a counters run of the same workload
     _, st, _, _ = h.run(source, args.policy, param, out=out, stats=True, seed=args.seed)
-    b_extract = 8 * st["queue_scanned"]
+    b_extract = 8 * st["queue_scanned"] + 8 * st["dense_scanned"]
     b_relax = 8 * st["extracted"] + 16 * st["edges"]
     b_touched = b_extract + b_relax
     kern_avg = statistics.mean(kern_ms)
@@ -295,7 +295,8 @@ def main():
                        "traffic": traffic, "peak_source": peak_src,
                        "frac_of_8TBps": achieved / 8000.0,
                        "algorithmic_bytes_per_launch": b_touched,
-                       "bytes_formula": "8*sum|Q_r| + 8*sum|F_r| + 16*sum E_r (SURVEY 8(d) B_touched)",
+                       "bytes_formula": "8*(ids scanned by Extract + vertices read by near/far dense passes) + 8*sum|F_r| "
+                                           "+ 16*sum E_r (SURVEY 8(d) B_touched; DESIGN.md §5)",
                        "traffic_source": traffic_src},
           "cpu_baseline": cpu,
           "e2e": {"value": e2e, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * g.n,
@@ -304,7 +305,7 @@ def main():
           "gpu_launches": args.steps,
           "clocks": clocks,
           "counters": {k: st[k] for k in ("rounds", "extracted", "edges", "succ", "inserts", "queue_scanned",
-                                          "max_queue", "max_frontier")}})
+                                          "dense_scanned", "max_queue", "max_frontier")}})
     if ws > 1:
         dist.destroy_process_group()
 

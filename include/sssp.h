@@ -97,6 +97,8 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t *d_offsets, const in
                                  and every frontier vertex relaxes with its key at Extract (reading R8).
                                  Default ("live"): light vertices relax while Extract is still running,
                                  fewer barriers; distances are identical, round counts may differ.     */
+#define SSSP_RUN_NO_NEARFAR 16u /* rho: list all of Q in the queue array every round instead of only
+                                   its near part (keys <= split; DESIGN.md §5 near/far)              */
 
 typedef struct {
     uint32_t flags;
@@ -120,8 +122,8 @@ typedef struct {
     int64_t t_theta_ns;   /* device time of ExtDist (globaltimer, CTA 0 view)          */
     int64_t t_extract_ns; /* device time of Extract (+ fused light relax)             */
     int64_t t_relax_ns;   /* device time of the remaining relax phase                 */
-    int64_t reserved0;
-    int64_t reserved1;
+    int64_t qnear;        /* ids listed in the queue array (near part of Q) and scanned  */
+    int64_t dense;        /* vertices read by near/far dense passes this round           */
 } sssp_round;
 
 typedef struct {
@@ -133,6 +135,7 @@ typedef struct {
     int64_t queue_scanned;  /* sum |Q_r|          (STATS only)                  */
     int64_t max_queue;      /* max |Q_r|          (STATS only)                  */
     int64_t max_frontier;   /* max |F_r|          (STATS only)                  */
+    int64_t dense_scanned;  /* sum of near/far dense-pass vertex reads (STATS)  */
     int32_t grid_blocks;    /* persistent-kernel CTAs                           */
     int32_t block_threads;  /* threads per CTA                                  */
     double kernel_ms;       /* device time of the round-loop launch (CUDA events on the handle's stream) */

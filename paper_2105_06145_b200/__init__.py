@@ -31,7 +31,7 @@ SSSP_RHO, SSSP_DELTA, SSSP_BELLMAN_FORD, SSSP_DIJKSTRA = 0, 1, 2, 3
 POLICIES = {"rho": SSSP_RHO, "delta": SSSP_DELTA, "bellman_ford": SSSP_BELLMAN_FORD, "bf": SSSP_BELLMAN_FORD,
             "dijkstra": SSSP_DIJKSTRA}
 SSSP_VALIDATE = 1
-SSSP_RUN_RHO_EXACT, SSSP_RUN_NO_WARMUP, SSSP_RUN_STATS, SSSP_RUN_SNAPSHOT = 1, 2, 4, 8
+SSSP_RUN_RHO_EXACT, SSSP_RUN_NO_WARMUP, SSSP_RUN_STATS, SSSP_RUN_SNAPSHOT, SSSP_RUN_NO_NEARFAR = 1, 2, 4, 8, 16
 SSSP_SELECT_SAMPLED, SSSP_SELECT_EXACT = 0, 1
 
 
@@ -52,7 +52,8 @@ class sssp_run_opts(ctypes.Structure):
 class sssp_run_stats(ctypes.Structure):
     _fields_ = [("rounds", ctypes.c_int64), ("extracted", ctypes.c_int64), ("edges", ctypes.c_int64),
                 ("succ", ctypes.c_int64), ("inserts", ctypes.c_int64), ("queue_scanned", ctypes.c_int64),
-                ("max_queue", ctypes.c_int64), ("max_frontier", ctypes.c_int64), ("grid_blocks", ctypes.c_int32),
+                ("max_queue", ctypes.c_int64), ("max_frontier", ctypes.c_int64), ("dense_scanned", ctypes.c_int64),
+                ("grid_blocks", ctypes.c_int32),
                 ("block_threads", ctypes.c_int32), ("kernel_ms", ctypes.c_double)]
 
     def as_dict(self):
@@ -60,7 +61,7 @@ class sssp_run_stats(ctypes.Structure):
 
 
 ROUND_FIELDS = ["qsize", "fsize", "edges", "inserts", "succ", "theta", "nheavy", "t_theta_ns", "t_extract_ns",
-                "t_relax_ns", "reserved0", "reserved1"]
+                "t_relax_ns", "qnear", "dense"]
 ROUND_WORDS = len(ROUND_FIELDS)
 
 _vp, _i32, _i64, _u64, _u32, _sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
@@ -154,7 +155,7 @@ class SSSP:
         return SSSP(off, idx, w, validate=validate)
 
     def run(self, source, policy="rho", param=0, out=None, stats=False, trace_cap=0, ext_counts=False,
-            exact=False, warmup=True, seed=0, max_rounds=0, snapshot=False):
+            exact=False, warmup=True, seed=0, max_rounds=0, snapshot=False, nearfar=True):
         """Alg. 1 from `source`; returns a uint64-valued int64 tensor of distances (INF = -1 as int64).
 
         With stats=True returns (dist, stats_dict, trace ndarray | None, ext_count tensor | None)."""
@@ -164,7 +165,8 @@ class SSSP:
             out = torch.empty(self.n, dtype=torch.int64, device=self.offsets.device)
         o = sssp_run_opts()
         o.flags = (SSSP_RUN_RHO_EXACT if exact else 0) | (0 if warmup else SSSP_RUN_NO_WARMUP) | \
-                  (SSSP_RUN_STATS if (stats or trace_cap) else 0) | (SSSP_RUN_SNAPSHOT if snapshot else 0)
+                  (SSSP_RUN_STATS if (stats or trace_cap) else 0) | (SSSP_RUN_SNAPSHOT if snapshot else 0) | \
+                  (0 if nearfar else SSSP_RUN_NO_NEARFAR)
         o.seed = seed
         o.max_rounds = max_rounds
         trace = None

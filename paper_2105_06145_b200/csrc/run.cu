@@ -64,13 +64,21 @@ constexpr int kLight = SSSP_LIGHT;           // out-degree <= kLight: relaxed by
 constexpr int kSmemSamples = 4096;           // theta samples held in shared memory (else CTA-0 fallback)
 constexpr int kRankSelect = 256;             // s <= this: select by rank counting
 constexpr int kWarps = kBlock / 32;
-constexpr int kEnt = 4;                      // queue entries per lane per Extract step
+#ifndef SSSP_NEAR_K
+#define SSSP_NEAR_K 4
+#endif
+#ifndef SSSP_ENT
+#define SSSP_ENT 4
+#endif
+constexpr int kEnt = SSSP_ENT;               // queue entries per lane per Extract step (large queues)
 constexpr int kQBuf = 256;                   // staged queue ids per warp (>= 32 * kArcs)
-constexpr int kLBuf = 32 * kEnt + 32;        // staged light vertices per warp
+constexpr int kTBuf = 32 * kEnt + 32;        // staged extracted ids per warp
 constexpr int kShards = 32;                  // append-list segments (+1 spill)
 constexpr int kSeg = kShards + 1;
 constexpr int kCntStride = 256;              // int32 words between counters (1 KB: distinct L2 slices)
 constexpr int kMaxCtas = 4096;
+constexpr int kNearK = SSSP_NEAR_K;          // near queue target: ~kNearK rounds of extraction
+constexpr int kFarSamples = 1024;            // vertices probed to place a new near/far split
 static_assert(32 * kArcs <= kQBuf, "one relax step must fit the stage");
 static_assert(kBlock % 32 == 0 && kBlock <= 1024, "block size");
 
@@ -89,8 +97,9 @@ struct __align__(128) RoundCnt {
     unsigned long long fsize;    // STATS: extracted
     unsigned long long edges;    // STATS: arcs of extracted vertices
     unsigned long long succ;     // STATS: successful WriteMins
-    unsigned long long inserts;  // STATS: ids appended by relax
-    unsigned long long pad[10];
+    unsigned long long inserts;  // STATS: ids inserted into Q by relax
+    unsigned long long split;    // CTA-0 broadcast of a new near/far split
+    unsigned long long pad[9];
 };
 
 struct __align__(128) Ctrl {
@@ -99,7 +108,7 @@ struct __align__(128) Ctrl {
     int32_t status;
     int32_t pad1;
     int64_t rounds;
-    int64_t tot_extracted, tot_edges, tot_succ, tot_inserts, tot_qscan, max_q, max_f;
+    int64_t tot_extracted, tot_edges, tot_succ, tot_inserts, tot_qscan, max_q, max_f, tot_dense;
 };
 
 // A sharded append list: segment s < kShards holds [s*cap, s*cap + min(count_s, cap)),
@@ -130,6 +139,7 @@ struct RunParams {
     int64_t ccap;       // per-shard chunk capacity
     int32_t* counters;  // [3 slots][2 lists: queue, chunks][kSeg] * kCntStride
     uint64_t* cta_min;  // [3 slots][kMaxCtas]: per-CTA min for Delta / Dijkstra
+    int64_t* cta_delta; // [3 slots][kMaxCtas]: per-CTA change of |Q| (inserts - extractions)
     Desc* light;
     uint64_t* samples;
     Ctrl* ctrl;
@@ -161,6 +171,7 @@ __device__ __forceinline__ void reset_cnt(RoundCnt* c) {
     c->edges = 0;
     c->succ = 0;
     c->inserts = 0;
+    c->split = 0;
 }
 
 __device__ __forceinline__ Desc ld_desc(const Desc* p) {
@@ -228,8 +239,8 @@ __device__ __forceinline__ int seg_of(const int64_t* pref, int64_t i) {
 
 // --------------------------------------------------------------------- per-warp staging
 struct WarpStage {
-    Desc light[kLBuf];
-    int32_t q[kQBuf];
+    int32_t take[kTBuf];  // ids that pass the theta test, extracted 32 at a time
+    int32_t q[kQBuf];     // ids appended to the next queue
 };
 
 struct Acc {
@@ -238,15 +249,29 @@ struct Acc {
     uint32_t inserts = 0;
 };
 
-struct Warp {  // per-warp working state (qn, ln are warp-uniform)
+struct Warp {  // per-warp working state (qn is warp-uniform)
     WarpStage* st;
     Sharded<int32_t> qnext;
     RoundCnt* C;
+    uint64_t split;  // near/far split: keys <= split are held in the queue array
+    int64_t qdelta;  // this lane's inserts - extractions (|Q| bookkeeping)
     int shard;
     int32_t qn;
-    int32_t ln;
     Acc acc;
 };
+
+// A successful WriteMin replaced word w_old by value c (flag cleared).  Returns true iff
+// v must be appended to the near queue: it was outside Q (insertion) and c <= split, or
+// it was a far member of Q (value > split) that now falls into the near range.
+template <bool STATS>
+__device__ __forceinline__ bool admit(uint64_t w_old, uint64_t c, Warp& W) {
+    if (w_old & kTop) {
+        W.qdelta++;
+        if (STATS) W.acc.inserts++;
+        return c <= W.split;
+    }
+    return (w_old & kVal) > W.split && c <= W.split;
+}
 
 // Reserve `tot` slots of a sharded list for this warp (lane 0 does the atomics).
 // Element i < tot goes to p0 + i if i < fit, else to p1 + (i - fit) (spill segment).
@@ -296,13 +321,13 @@ __device__ __forceinline__ void wq_push1(Warp& W, bool pred, int32_t id) {
 // WriteMin(delta[v], c) on the packed word, given a prior read `w`.
 // Returns true iff this lane inserted v into Q (its flag bit was set) and must append it.
 template <int POL, bool STATS>
-__device__ __forceinline__ bool write_min(uint64_t* dist, int32_t v, uint64_t c, uint64_t w, Acc& acc) {
+__device__ __forceinline__ bool write_min(uint64_t* dist, int32_t v, uint64_t c, uint64_t w, Warp& W) {
     while ((w & kVal) > c) {
         const uint64_t old = atomicCAS((unsigned long long*)(dist + v), (unsigned long long)w, (unsigned long long)c);
         if (old == w) {
-            if (STATS) acc.succ++;
-            if (uses_min(POL)) acc.minsucc = c < acc.minsucc ? c : acc.minsucc;
-            return (w & kTop) != 0;
+            if (STATS) W.acc.succ++;
+            if (uses_min(POL)) W.acc.minsucc = c < W.acc.minsucc ? c : W.acc.minsucc;
+            return admit<STATS>(w, c, W);
         }
         w = old;
     }
@@ -334,9 +359,9 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
             if (old[t] == cur[t]) {
                 if (STATS) W.acc.succ++;
                 if (uses_min(POL)) W.acc.minsucc = c[t] < W.acc.minsucc ? c[t] : W.acc.minsucc;
-                app[t] = (cur[t] & kTop) != 0;
+                app[t] = admit<STATS>(cur[t], c[t], W);
             } else {
-                app[t] = write_min<POL, STATS>(p.dist, v[t], c[t], old[t], W.acc);
+                app[t] = write_min<POL, STATS>(p.dist, v[t], c[t], old[t], W);
             }
         } else {
             app[t] = false;
@@ -352,7 +377,6 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
     for (int t = 0; t < kArcs; t++)
         if (app[t]) W.st->q[pos++] = v[t];
     W.qn += tot;
-    if (STATS) W.acc.inserts += cnt;
 }
 
 // One chunk: arcs [beg, beg+len) of a vertex with key d, len <= kChunk.  Lane-strided
@@ -402,51 +426,6 @@ __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, i
     }
 }
 
-// Stage light vertices (live mode); light_relax_full relaxes them 32 at a time.
-__device__ __forceinline__ void light_stage(bool pred, uint64_t d, int32_t beg, int32_t deg, Warp& W) {
-    const uint32_t mask = __ballot_sync(kFull, pred);
-    if (!mask) return;
-    if (pred) st_desc_smem(&W.st->light[W.ln + __popc(mask & lanemask_lt())], d, beg, deg);
-    W.ln += __popc(mask);
-}
-
-template <int POL, bool STATS>
-__device__ __forceinline__ void light_relax_full(const RunParams& p, Warp& W) {
-    const int lane = lane_id();
-    int32_t done = 0;
-    while (W.ln - done >= 32) {
-        __syncwarp();
-        const Desc e = W.st->light[done + lane];
-        done += 32;
-        relax_vertices<POL, STATS>(p, e.d, e.beg, e.len, W);
-    }
-    if (done) {  // move the remainder (< 32) to the front
-        __syncwarp();
-        const bool mv = lane < W.ln - done;
-        Desc t;
-        if (mv) t = W.st->light[done + lane];
-        __syncwarp();
-        if (mv) W.st->light[lane] = t;
-        __syncwarp();
-        W.ln -= done;
-    }
-}
-
-template <int POL, bool STATS>
-__device__ __forceinline__ void light_drain(const RunParams& p, Warp& W) {
-    if (W.ln == 0) return;
-    __syncwarp();
-    const int lane = lane_id();
-    Desc e;
-    e.d = 0;
-    e.beg = 0;
-    e.len = 0;
-    if (lane < W.ln) e = W.st->light[lane];
-    __syncwarp();
-    W.ln = 0;
-    relax_vertices<POL, STATS>(p, e.d, e.beg, e.len, W);
-}
-
 // Cut the heavy lanes' vertices into kChunk-arc descriptors (one reservation per warp).
 __device__ __forceinline__ void emit_chunks(const Sharded<Desc>& CL, int shard, bool heavy, uint64_t d, int32_t beg,
                                             int32_t deg, RoundCnt* C, bool stats) {
@@ -481,18 +460,59 @@ __device__ __forceinline__ void emit_chunks(const Sharded<Desc>& CL, int shard, 
 }
 
 // --------------------------------------------------------------------- phase A
-// Extract(theta): kEnt queue entries per lane per step, all loads issued together.
-template <int POL, bool STATS, bool SNAP>
+// Extract(theta) in two decoupled parts:
+//  scan:  kEnt queue entries per lane per step (all id loads, then all key gathers in
+//         flight); ids above theta are staged for the next queue, ids at or below it
+//         are staged in the warp's take buffer;
+//  batch: 32 staged ids at a time are deleted from Q (atomicOr, which returns the exact
+//         key they relax with), their CSR rows read, heavy ones cut into chunks and the
+//         light ones relaxed by the warp at once (live) or listed (snapshot).
+template <int POL, bool STATS>
+__device__ __forceinline__ void take_batch(const RunParams& p, int32_t cnt, const Sharded<Desc>& CL, bool snap, Warp& W,
+                                           uint64_t& fs, uint64_t& edges) {
+    const int lane = lane_id();
+    __syncwarp();
+    int32_t id = lane < cnt ? W.st->take[lane] : -1;
+    uint64_t d = 0;
+    int32_t beg = 0, deg = 0;
+    if (id >= 0) {
+        const uint64_t old = atomicOr((unsigned long long*)(p.dist + id), (unsigned long long)kTop);  // delete from Q
+        d = old & kVal;
+        if (old & kTop) id = -1;  // already deleted by another copy (safety net: copies are not expected)
+    }
+    if (id >= 0) {
+        W.qdelta--;
+        beg = __ldg(p.off + id);
+        deg = __ldg(p.off + id + 1) - beg;
+        if (p.ext_count) atomicAdd(p.ext_count + id, 1);
+    }
+    if (STATS && id >= 0) {
+        fs += 1;
+        edges += (uint64_t)deg;
+    }
+    const bool heavy = deg > kLight;
+    const bool light = id >= 0 && deg > 0 && !heavy;
+    emit_chunks(CL, W.shard, heavy, d, beg, deg, W.C, STATS);
+    if (snap) {
+        const int32_t ls = warp_append_slot(light, &W.C->nlight);
+        if (light) st_desc(p.light + ls, d, beg, deg);
+    } else if (__any_sync(kFull, light)) {
+        relax_vertices<POL, STATS>(p, d, beg, light ? deg : 0, W);
+    }
+}
+
+template <int POL, bool STATS>
 __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_t>& QC, const int64_t* qpref,
-                                        const Sharded<Desc>& CL, uint64_t theta, uint64_t& minrem, Warp& W) {
+                                        const Sharded<Desc>& CL, uint64_t theta, bool snap, uint64_t& minrem, Warp& W) {
     const int lane = lane_id();
     const int64_t q = qpref[kSeg];
     const int64_t gw = warp_rank();
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     uint64_t fs = 0, edges = 0;
+    int32_t tn = 0;  // staged take ids (warp-uniform)
     // kEnt entries per lane only when every warp gets at least two such steps; small
     // queues are spread one entry per lane so that more warps share the round
-    const int ent = q >= nwarps * (64 * kEnt) ? kEnt : 1;
+    const int ent = q >= nwarps * (32 * kEnt) ? kEnt : 1;
     for (int64_t base = gw * (32 * ent); base < q; base += nwarps * (32 * ent)) {
         int32_t id[kEnt];
         uint64_t val[kEnt];
@@ -509,44 +529,38 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
         }
 #pragma unroll
         for (int e = 0; e < kEnt; e++) val[e] = id[e] >= 0 ? (ld_cg_u64(p.dist + id[e]) & kVal) : kVal;
-        int32_t beg[kEnt], deg[kEnt];
 #pragma unroll
         for (int e = 0; e < kEnt; e++) {
-            beg[e] = 0;
-            deg[e] = 0;
-            if (id[e] >= 0 && val[e] <= theta) {
-                // delete u from Q; the returned word is u's key at deletion (<= val)
-                val[e] = atomicOr((unsigned long long*)(p.dist + id[e]), (unsigned long long)kTop) & kVal;
-                beg[e] = __ldg(p.off + id[e]);
-                deg[e] = __ldg(p.off + id[e] + 1) - beg[e];
-                if (p.ext_count) atomicAdd(p.ext_count + id[e], 1);
-            } else if (id[e] >= 0) {
-                deg[e] = -1;  // stays in Q
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < kEnt; e++) {
-            const bool rem = deg[e] < 0;
-            const bool take = id[e] >= 0 && !rem;
-            wq_push1(W, rem, id[e]);
+            const bool take = id[e] >= 0 && val[e] <= theta;
+            const bool rem = id[e] >= 0 && !take;
+            wq_push1(W, rem && val[e] <= W.split, id[e]);  // above the split: stays in Q as a far member
             if (uses_min(POL) && rem) minrem = val[e] < minrem ? val[e] : minrem;
-            if (STATS && take) {
-                fs += 1;
-                edges += (uint64_t)deg[e];
-            }
-            const bool heavy = take && deg[e] > kLight;
-            const bool light = take && deg[e] > 0 && !heavy;
-            emit_chunks(CL, W.shard, heavy, val[e], beg[e], deg[e], W.C, STATS);
-            if (SNAP) {
-                const int32_t ls = warp_append_slot(light, &W.C->nlight);
-                if (light) st_desc(p.light + ls, val[e], beg[e], deg[e]);
-            } else {
-                light_stage(light, val[e], beg[e], deg[e], W);
-            }
+            const uint32_t tm = __ballot_sync(kFull, take);
+            if (take) W.st->take[tn + __popc(tm & lanemask_lt())] = id[e];
+            tn += __popc(tm);
         }
-        if (!SNAP) light_relax_full<POL, STATS>(p, W);
+        int32_t done = 0;
+        while (tn - done >= 32) {
+            if (done) {  // move the next 32 to the front (take_batch reads take[0..32))
+                __syncwarp();
+                const int32_t x = W.st->take[done + lane];
+                __syncwarp();
+                W.st->take[lane] = x;
+            }
+            take_batch<POL, STATS>(p, 32, CL, snap, W, fs, edges);
+            done += 32;
+        }
+        if (done) {  // keep the remainder (< 32) at the front
+            __syncwarp();
+            const bool mv = lane < tn - done;
+            int32_t x = 0;
+            if (mv) x = W.st->take[done + lane];
+            __syncwarp();
+            if (mv) W.st->take[lane] = x;
+            tn -= done;
+        }
     }
-    if (!SNAP) light_drain<POL, STATS>(p, W);
+    if (tn) take_batch<POL, STATS>(p, tn, CL, snap, W, fs, edges);
     if (STATS) {
         fs = warp_sum(fs);
         edges = warp_sum(edges);
@@ -556,13 +570,13 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
 }
 
 // --------------------------------------------------------------------- phase B
-template <int POL, bool STATS, bool SNAP>
+template <int POL, bool STATS>
 __device__ __forceinline__ void phase_b(const RunParams& p, const Sharded<Desc>& CL, const int64_t* cpref, int32_t nl,
                                         Warp& W) {
     const int lane = lane_id();
     const int64_t gw = warp_rank();
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t nb = SNAP ? ((int64_t)nl + 31) / 32 : 0;
+    const int64_t nb = ((int64_t)nl + 31) / 32;
     const int64_t nc = cpref[kSeg];
     const int64_t total = nb + nc;
     auto chunk_at = [&](int64_t i) {  // i-th descriptor of the concatenated segments
@@ -573,7 +587,7 @@ __device__ __forceinline__ void phase_b(const RunParams& p, const Sharded<Desc>&
     Desc nxt;
     if (item >= nb && item < total) nxt = chunk_at(item - nb);
     for (; item < total; item += nwarps) {
-        if (SNAP && item < nb) {
+        if (item < nb) {
             const int64_t j = item * 32 + lane;
             Desc e;
             if (j < nl) {
@@ -594,8 +608,12 @@ __device__ __forceinline__ void phase_b(const RunParams& p, const Sharded<Desc>&
 }
 
 template <int POL, bool STATS>
-__device__ __forceinline__ void flush_acc(Warp& W) {
+__device__ __forceinline__ void flush_acc(const RunParams& p, int64_t r, Warp& W) {
     wq_flush(W);
+    const int64_t dq = warp_sum(W.qdelta);
+    if (lane_id() == 0 && dq) atomicAdd((unsigned long long*)(p.cta_delta + (r % 3) * kMaxCtas + blockIdx.x),
+                                        (unsigned long long)dq);
+    W.qdelta = 0;
     if (STATS) {
         const uint32_t s = warp_sum(W.acc.succ), ins = warp_sum(W.acc.inserts);
         if (lane_id() == 0 && s) atomicAdd(&W.C->succ, (unsigned long long)s);
@@ -655,24 +673,78 @@ __device__ __forceinline__ uint64_t cta_kth_by_rank(const uint64_t* keys, int s,
     return th;
 }
 
+// --------------------------------------------------------------------- near/far queue
+// The queue array holds only the NEAR members of Q (key <= split); FAR members (key >
+// split) are implicit: their flag bit says "in Q" and nothing else lists them.  When the
+// near part runs low, a coalesced dense pass over delta moves the FAR keys in (split,
+// split'] into the queue (DESIGN.md §5 "near/far").  Rounds then rescan ~kNearK rounds
+// of work instead of all of Q.
+
+// Dense pass: append every far member with value in (lo, hi] to the list L (staged).
+__device__ __forceinline__ void far_to_near(const RunParams& p, const Sharded<int32_t>& L, uint64_t lo, uint64_t hi,
+                                            Warp& W) {
+    const int lane = lane_id();
+    const Sharded<int32_t> saved = W.qnext;
+    W.qnext = L;
+    const int64_t gw = warp_rank();
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    constexpr int kV = 8;
+    for (int64_t base = gw * (32 * kV); base < p.n; base += nwarps * (32 * kV)) {
+        uint64_t x[kV];
+#pragma unroll
+        for (int t = 0; t < kV; t++) {
+            const int64_t v = base + t * 32 + lane;
+            x[t] = v < p.n ? __ldcg((const unsigned long long*)(p.dist + v)) : kInf;
+        }
+#pragma unroll
+        for (int t = 0; t < kV; t++) {
+            const uint64_t val = x[t] & kVal;
+            wq_push1(W, !(x[t] & kTop) && val > lo && val <= hi, (int32_t)(base + t * 32 + lane));
+        }
+    }
+    wq_flush(W);
+    W.qnext = saved;
+}
+
+// CTA-0 estimate of the value below which about `want` far members lie: rejection-sample
+// vertices, keep the far ones, take the matching order statistic (kInf if none seen).
+__device__ uint64_t far_quantile(const RunParams& p, uint64_t split, int64_t far, int64_t want, int64_t r,
+                                 uint64_t* keys, SelectSmem& sm, int32_t* cnt) {
+    if (threadIdx.x == 0) *cnt = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < kFarSamples; j += blockDim.x) {
+        const uint64_t v = splitmix64(p.seed ^ 0xF00DF00DF00DULL ^ splitmix64(((uint64_t)r << 32) | (uint64_t)j)) %
+                           (uint64_t)p.n;
+        const uint64_t x = __ldcg((const unsigned long long*)(p.dist + v));
+        if (!(x & kTop) && (x & kVal) > split) keys[atomicAdd(cnt, 1)] = x & kVal;
+    }
+    __syncthreads();
+    const int32_t h = *cnt;
+    if (h == 0) return kInf;
+    uint64_t k = (uint64_t)(((double)want / (double)far) * h) + 1;
+    k = k > (uint64_t)h ? (uint64_t)h : k;
+    return h <= kRankSelect ? cta_kth_by_rank(keys, h, k, sm) : cta_kth_smallest(SmemKey{keys}, h, k, sm);
+}
+
 // --------------------------------------------------------------------- the round loop
-template <int POL, bool STATS, bool SNAP>
+template <int POL, bool STATS>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpStage* stage = (WarpStage*)smem_raw;                                // [kWarps]
     uint64_t* s_keys = (uint64_t*)(smem_raw + kWarps * sizeof(WarpStage));  // [kSmemSamples]
     SelectSmem& sm = *(SelectSmem*)(s_keys + kSmemSamples);
-    __shared__ int64_t qpref[kSeg + 1];  // segment prefix of Q_r
+    __shared__ int64_t qpref[kSeg + 1];  // segment prefix of Q_r's near part
     __shared__ int64_t cpref[kSeg + 1];  // segment prefix of the round's chunk list
-    __shared__ uint64_t bc_u[2];         // min_Q (Delta / Dijkstra), CTA-0 theta
-    __shared__ int32_t bc_nl;
+    __shared__ uint64_t bc_u[3];         // min_Q (Delta / Dijkstra), CTA-0 theta, CTA-0 split
+    __shared__ int64_t bc_dq;
+    __shared__ int32_t bc_nl, bc_cnt;
     __shared__ uint64_t red[kWarps];
     Ctrl* ctrl = p.ctrl;
     Warp W;
     W.st = stage + (threadIdx.x >> 5);
     W.shard = (int)(warp_rank() % kShards);
     W.qn = 0;
-    W.ln = 0;
+    W.qdelta = 0;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
 
@@ -681,7 +753,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     if (p.ext_count)
         for (int64_t i = gtid; i < p.n; i += gsize) p.ext_count[i] = 0;
     for (int64_t i = gtid; i < 3 * 2 * kSeg; i += gsize) p.counters[i * kCntStride] = 0;
-    for (int64_t i = gtid; i < 3 * kMaxCtas; i += gsize) p.cta_min[i] = kInf;
+    for (int64_t i = gtid; i < 3 * kMaxCtas; i += gsize) {
+        p.cta_min[i] = kInf;
+        p.cta_delta[i] = 0;
+    }
     if (gtid == 0) {
         p.qbuf[1][0] = p.source;  // Q_1 lives in qbuf[1], shard 0
         for (int c = 0; c < 3; c++) reset_cnt(&ctrl->cnt[c]);
@@ -689,6 +764,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         ctrl->rounds = 0;
         ctrl->tot_extracted = ctrl->tot_edges = ctrl->tot_succ = ctrl->tot_inserts = 0;
         ctrl->tot_qscan = ctrl->max_q = ctrl->max_f = 0;
+        ctrl->tot_dense = 0;
     }
     grid_sync(nullptr);
     if (gtid == 0) {
@@ -697,6 +773,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     }
     grid_sync(nullptr);
 
+    // near/far queue for rho only (Delta* / BF / Dijkstra keep split = +inf: all of Q listed)
+    const bool nearfar = POL == SSSP_RHO && !(p.flags & SSSP_RUN_NO_NEARFAR);
+    uint64_t split = kInf;  // near/far split (uniform across the grid)
+    int64_t qtot = 1;       // |Q_r| = near + far
     uint64_t theta_prev = 0;
     int warm = 0;
     int64_t r = 1;
@@ -704,24 +784,40 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         RoundCnt* C = &ctrl->cnt[r % 3];
         const Sharded<int32_t> QC = queue_of(p, r);
         const Sharded<Desc> CL = chunks_of(p, r);
-        load_prefix(QC, qpref);
-        const int64_t q = qpref[kSeg];  // |Q_r|
-        if (q == 0) break;              // while |Q| > 0
+        // |Q_r| = |Q_{r-1}| + sum over CTAs of (inserts - extractions) in round r-1
+        if ((threadIdx.x >> 5) == 1 && r > 1) {  // warp 1, in parallel with warp 0's load_prefix
+            const int lane = lane_id();
+            const int64_t* cd = p.cta_delta + ((r + 2) % 3) * kMaxCtas;
+            int64_t sdq = 0;
+            for (int i = lane; i < (int)gridDim.x; i += 32) sdq += __ldcg((const long long*)(cd + i));
+            sdq = warp_sum(sdq);
+            if (lane == 0) bc_dq = sdq;
+        }
+        load_prefix(QC, qpref);  // ends with __syncthreads
+        if (r > 1) qtot += bc_dq;
+        int64_t qn = qpref[kSeg];  // near part of Q_r
+        if (qtot == 0) break;      // while |Q| > 0
         if (r > p.max_rounds) {
             if (gtid == 0) ctrl->status = SSSP_ERR_ROUNDS;
             break;
         }
         uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+        int64_t dense = 0;
         if (STATS && gtid == 0) t0 = globaltimer();
         if (gtid == 0) reset_cnt(&ctrl->cnt[(r + 1) % 3]);
         if (gtid < 2 * kSeg) {  // counters of slot (r+1)%3: written in round r+1, read in r+1 / r+2
             p.counters[((int64_t)(((r + 1) % 3) * 2) * kSeg + gtid) * kCntStride] = 0;
         }
+        if (threadIdx.x == 0) p.cta_delta[((r + 1) % 3) * kMaxCtas + blockIdx.x] = 0;
         W.qnext = queue_of(p, r + 1);
         W.C = C;
 
-        // ---- ExtDist (Table tab:framework)
+        // ---- ExtDist (Table tab:framework) and near/far maintenance
         uint64_t theta;
+        // A round that lowers the split runs snapshot-style (Extract finishes before any
+        // relax): a live relax could not tell a near id still listed from one Extract
+        // just moved to the far part (DESIGN.md §5 near/far).
+        bool snap = (p.flags & SSSP_RUN_SNAPSHOT) != 0;
         if (POL == SSSP_BELLMAN_FORD) {
             theta = kInf;
         } else if (POL == SSSP_DIJKSTRA || POL == SSSP_DELTA) {
@@ -749,20 +845,72 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             }
         } else {  // rho
             uint64_t rho = p.param;
-            if (!(p.flags & SSSP_RUN_NO_WARMUP) && (uint64_t)q > rho && warm < 2) {
+            if (!(p.flags & SSSP_RUN_NO_WARMUP) && (uint64_t)qtot > rho && warm < 2) {
                 warm++;
                 rho = rho / 10 ? rho / 10 : 1;  // reading R7
             }
-            const uint64_t s = sample_count((uint64_t)q, rho);
+            const uint64_t want = rho > kInf / (4 * kNearK) ? kInf / 4 : (uint64_t)kNearK * rho;
+            // pull far keys in until the near part holds the rho smallest of Q (or all of Q)
+            for (int it = 0; nearfar && qtot > qn && ((uint64_t)qtot <= rho || (uint64_t)qn < rho); it++) {
+                uint64_t hi = kInf;
+                if ((uint64_t)qtot > rho && it < 3) {
+                    if (blockIdx.x == 0) {
+                        const uint64_t tgt = want > kInf >> 4 ? want : want << it;
+                        int64_t need = tgt >= (uint64_t)qtot ? qtot : (int64_t)tgt - qn;
+                        need = need < 1 ? 1 : need;
+                        const uint64_t h = need >= qtot - qn ? kInf
+                                                             : far_quantile(p, split, qtot - qn, need, r * 4 + it,
+                                                                            s_keys, sm, &bc_cnt);
+                        if (threadIdx.x == 0) C->split = h;
+                    }
+                    grid_sync(nullptr);
+                    if (threadIdx.x == 0) bc_u[2] = __ldcg((const unsigned long long*)&C->split);
+                    __syncthreads();
+                    hi = bc_u[2];
+                }
+                far_to_near(p, QC, split, hi, W);
+                dense += p.n;
+                grid_sync(nullptr);
+                load_prefix(QC, qpref);
+                qn = qpref[kSeg];
+                split = hi;
+            }
             const QueueVal qv{QC, qpref, p.dist};
-            if ((uint64_t)q <= rho) {
-                theta = kInf;  // |Q| <= rho: extract all (P:1376)
-            } else if (!(p.flags & SSSP_RUN_RHO_EXACT) && s <= (uint64_t)kSmemSamples) {
-                // every CTA draws the same samples and selects the same theta: no barrier
-                for (uint64_t j = threadIdx.x; j < s; j += blockDim.x)
-                    s_keys[j] = qv((int64_t)sample_index(p.seed, r, j, (uint64_t)q));
+            if (nearfar && (uint64_t)qn > 4 * want && qn > (int64_t)(p.n >> 5)) {
+                // the near part grew far beyond the target: lower the split to about the
+                // want-th smallest near key (CTA 0 + broadcast keeps it grid-uniform);
+                // Extract then leaves the near ids above it to the far part
+                if (blockIdx.x == 0) {
+                    uint64_t s2 = sample_count((uint64_t)qn, want);
+                    s2 = s2 > (uint64_t)kSmemSamples ? (uint64_t)kSmemSamples : s2;
+                    for (uint64_t j = threadIdx.x; j < s2; j += blockDim.x)
+                        s_keys[j] = qv((int64_t)sample_index(p.seed ^ 0x5EED5EEDull, r, j, (uint64_t)qn));
+                    __syncthreads();
+                    uint64_t k = (want * s2 + (uint64_t)qn - 1) / (uint64_t)qn;
+                    k = k < 1 ? 1 : (k > s2 ? s2 : k);
+                    const uint64_t h = cta_kth_smallest(SmemKey{s_keys}, (int64_t)s2, k, sm);
+                    if (threadIdx.x == 0) C->split = h;
+                }
+                grid_sync(nullptr);
+                if (threadIdx.x == 0) bc_u[2] = __ldcg((const unsigned long long*)&C->split);
                 __syncthreads();
-                uint64_t k = (rho * s + (uint64_t)q - 1) / (uint64_t)q;
+                if (bc_u[2] < split) {
+                    split = bc_u[2];
+                    snap = true;
+                }
+            }
+            const uint64_t s = sample_count((uint64_t)qn, rho);
+            if ((uint64_t)qtot <= rho) {
+                theta = kInf;  // |Q| <= rho: extract all (P:1376)
+            } else if ((uint64_t)qn < rho) {
+                theta = split;  // (near part short of rho after the pulls: extract all of it)
+            } else if (!(p.flags & SSSP_RUN_RHO_EXACT) && s <= (uint64_t)kSmemSamples) {
+                // every CTA draws the same samples of the near part (which holds the rho
+                // smallest keys of Q) and selects the same theta: no barrier
+                for (uint64_t j = threadIdx.x; j < s; j += blockDim.x)
+                    s_keys[j] = qv((int64_t)sample_index(p.seed, r, j, (uint64_t)qn));
+                __syncthreads();
+                uint64_t k = (rho * s + (uint64_t)qn - 1) / (uint64_t)qn;
                 k = k < 1 ? 1 : (k > s ? s : k);
                 theta = s <= (uint64_t)kRankSelect ? cta_kth_by_rank(s_keys, (int)s, k, sm)
                                                    : cta_kth_smallest(SmemKey{s_keys}, (int64_t)s, k, sm);
@@ -770,12 +918,12 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                 if (blockIdx.x == 0) {
                     uint64_t th;
                     if (p.flags & SSSP_RUN_RHO_EXACT) {
-                        th = cta_kth_smallest(qv, q, rho, sm);
+                        th = cta_kth_smallest(qv, qn, rho, sm);
                     } else {
                         for (uint64_t j = threadIdx.x; j < s; j += blockDim.x)
-                            p.samples[j] = qv((int64_t)sample_index(p.seed, r, j, (uint64_t)q));
+                            p.samples[j] = qv((int64_t)sample_index(p.seed, r, j, (uint64_t)qn));
                         __syncthreads();
-                        uint64_t k = (rho * s + (uint64_t)q - 1) / (uint64_t)q;
+                        uint64_t k = (rho * s + (uint64_t)qn - 1) / (uint64_t)qn;
                         k = k < 1 ? 1 : (k > s ? s : k);
                         th = cta_kth_smallest(ArrayKey{p.samples}, (int64_t)s, k, sm);
                     }
@@ -787,21 +935,22 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                 theta = bc_u[1];
             }
         }
+        W.split = split;
         if (STATS && gtid == 0) t1 = globaltimer();
 
         // ---- phase A: Extract(theta) (+ light relax in live mode)
         uint64_t minrem = kInf;
-        phase_a<POL, STATS, SNAP>(p, QC, qpref, CL, theta, minrem, W);
-        flush_acc<POL, STATS>(W);
+        phase_a<POL, STATS>(p, QC, qpref, CL, theta, snap, minrem, W);
+        flush_acc<POL, STATS>(p, r, W);
         grid_sync(nullptr);
         if (STATS && gtid == 0) t2 = globaltimer();
         // ---- phase B: heavy chunks (+ light list in snapshot mode)
         load_prefix(CL, cpref);
-        if (threadIdx.x == 0) bc_nl = SNAP ? __ldcg(&C->nlight) : 0;
+        if (threadIdx.x == 0) bc_nl = snap ? __ldcg(&C->nlight) : 0;
         __syncthreads();
         const int32_t nl = bc_nl;
         const bool phase_b_work = cpref[kSeg] + nl > 0;
-        if (phase_b_work) phase_b<POL, STATS, SNAP>(p, CL, cpref, nl, W);
+        if (phase_b_work) phase_b<POL, STATS>(p, CL, cpref, nl, W);
         if (uses_min(POL)) {  // this CTA's min over kept ids and successful WriteMins
             uint64_t mn = warp_min_u64(minrem < W.acc.minsucc ? minrem : W.acc.minsucc);
             if (lane_id() == 0) red[threadIdx.x >> 5] = mn;
@@ -813,7 +962,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             W.acc.minsucc = kInf;
         }
         if (phase_b_work) {
-            flush_acc<POL, STATS>(W);
+            flush_acc<POL, STATS>(p, r, W);
             grid_sync(nullptr);
         } else if (uses_min(POL) || STATS) {
             grid_sync(nullptr);
@@ -824,7 +973,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             const int64_t f = (int64_t)C->fsize;
             if (p.trace && r - 1 < p.trace_cap) {
                 sssp_round* t = p.trace + (r - 1);
-                t->qsize = q;
+                t->qsize = qtot;
                 t->fsize = f;
                 t->edges = (int64_t)C->edges;
                 t->inserts = (int64_t)C->inserts;
@@ -834,15 +983,16 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                 t->t_theta_ns = (int64_t)(t1 - t0);
                 t->t_extract_ns = (int64_t)(t2 - t1);
                 t->t_relax_ns = (int64_t)(t3 - t2);
-                t->reserved0 = cpref[kSeg];
-                t->reserved1 = 0;
+                t->qnear = qn;
+                t->dense = dense;
             }
             ctrl->tot_extracted += f;
             ctrl->tot_edges += (int64_t)C->edges;
             ctrl->tot_succ += (int64_t)C->succ;
             ctrl->tot_inserts += (int64_t)C->inserts;
-            ctrl->tot_qscan += q;
-            ctrl->max_q = q > ctrl->max_q ? q : ctrl->max_q;
+            ctrl->tot_qscan += qn;
+            ctrl->tot_dense += dense;
+            ctrl->max_q = qtot > ctrl->max_q ? qtot : ctrl->max_q;
             ctrl->max_f = f > ctrl->max_f ? f : ctrl->max_f;
         }
     }
@@ -901,6 +1051,7 @@ struct Layout {
     int64_t ccap;
     int32_t* counters;
     uint64_t* cta_min;
+    int64_t* cta_delta;
     Desc* light;
     uint64_t* samples;
     Ctrl* ctrl;
@@ -922,6 +1073,7 @@ Layout carve(void* base, int32_t n, int64_t m) {
     L.err = c.take<int32_t>(32);
     L.counters = c.take<int32_t>((size_t)3 * 2 * kSeg * kCntStride);
     L.cta_min = c.take<uint64_t>((size_t)3 * kMaxCtas);
+    L.cta_delta = c.take<int64_t>((size_t)3 * kMaxCtas);
     L.dist = c.take<uint64_t>(n);
     L.q0 = c.take<int32_t>(qlen);
     L.q1 = c.take<int32_t>(qlen);
@@ -938,8 +1090,8 @@ constexpr size_t kSmemBytes = kWarps * sizeof(WarpStage) + kSmemSamples * sizeof
 
 template <int POL>
 KernelFn kernel_for_pol(bool stats, bool snap) {
-    if (stats) return snap ? sssp_round_loop<POL, true, true> : sssp_round_loop<POL, true, false>;
-    return snap ? sssp_round_loop<POL, false, true> : sssp_round_loop<POL, false, false>;
+    (void)snap;  // snapshot rounds are a runtime flag
+    return stats ? sssp_round_loop<POL, true> : sssp_round_loop<POL, false>;
 }
 
 KernelFn kernel_for(int pol, bool stats, bool snap) {
@@ -1012,6 +1164,7 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
     b.ccap = L.ccap;
     b.counters = L.counters;
     b.cta_min = L.cta_min;
+    b.cta_delta = L.cta_delta;
     b.light = L.light;
     b.samples = L.samples;
     b.ctrl = L.ctrl;
@@ -1111,6 +1264,7 @@ sssp_status sssp_run_ex(sssp_handle* h, int32_t source, sssp_policy policy, uint
         stats->queue_scanned = c->tot_qscan;
         stats->max_queue = c->max_q;
         stats->max_frontier = c->max_f;
+        stats->dense_scanned = c->tot_dense;
         stats->grid_blocks = grid;
         stats->block_threads = kBlock;
         float ms = 0.f;

@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--only", default=None, help="policy:param,... overrides the built-in sweep")
     ap.add_argument("--snapshot", action="store_true", help="deterministic (snapshot) rounds")
+    ap.add_argument("--no-nearfar", action="store_true", help="list all of Q every round (rho)")
     ap.add_argument("--trace", default=None, help="append per-round traces of the stats runs here (jsonl)")
     ap.add_argument("--tag", default=os.environ.get("SSSP_LIB", "default"))
     args = ap.parse_args()
@@ -59,24 +60,24 @@ def main():
         print(f"== {name}: n={g.n} m={g.m} src={g.source} gen {tg:.1f}s", flush=True)
         for pol, par in cases:
             snap = args.snapshot
+            kw = dict(snapshot=snap, nearfar=not args.no_nearfar, max_rounds=200000)
             for _ in range(2):
-                h.run(g.source, pol, par, out=d, snapshot=snap)
+                h.run(g.source, pol, par, out=d, **kw)
             ks, rs = [], []
             for r in range(args.reps):
                 flush.zero_()
-                h.run(g.source, pol, par, out=d, seed=r, snapshot=snap)
+                h.run(g.source, pol, par, out=d, seed=r, **kw)
                 ks.append(h.last_stats["kernel_ms"])
                 rs.append(h.last_stats["rounds"])
-            _, st, tr, _ = h.run(g.source, pol, par, out=d, stats=True, trace_cap=1 << 20 if args.trace else 0,
-                                 snapshot=snap)
+            _, st, tr, _ = h.run(g.source, pol, par, out=d, stats=True, trace_cap=1 << 20 if args.trace else 0, **kw)
             if args.trace and tr is not None:
                 with open(args.trace, "a") as f:
                     f.write(json.dumps({"config": name, "policy": pol, "param": par, "tag": args.tag,
                                         "snapshot": snap, "rounds": {k: tr[k].tolist() for k in tr.dtype.names}})
                             + "\n")
             km = statistics.median(ks)
-            bt = 8 * st["queue_scanned"] + 8 * st["extracted"] + 16 * st["edges"]
-            rec = {"config": name, "policy": pol, "param": par, "tag": args.tag, "snapshot": snap, "kernel_ms": km, "kernel_ms_min": min(ks),
+            bt = 8 * st["queue_scanned"] + 8 * st["dense_scanned"] + 8 * st["extracted"] + 16 * st["edges"]
+            rec = {"config": name, "policy": pol, "param": par, "tag": args.tag + ("/nonf" if args.no_nearfar else ""), "snapshot": snap, "kernel_ms": km, "kernel_ms_min": min(ks),
                    "gteps": g.m / km / 1e6, "rounds": statistics.median(rs), "stats_rounds": st["rounds"],
                    "bytes_touched": bt, "touched_gbs": bt / km / 1e6, "frac_6552": bt / km / 1e6 / 6552.6,
                    "edges_per_m": st["edges"] / g.m, "qscan_per_n": st["queue_scanned"] / g.n,

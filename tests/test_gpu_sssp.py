@@ -169,7 +169,8 @@ def test_round_trace_parity(cuda_device, name):
     h = P.SSSP.from_graph(g)
     cases = [("bellman_ford", 0, {}), ("delta", 1000, {}), ("delta", 20000, {}), ("dijkstra", 0, {}),
              ("rho", 64, dict(exact=True, warmup=False)), ("rho", 2048, dict(exact=True, warmup=False)),
-             ("rho", 512, dict(exact=True, warmup=True))]
+             ("rho", 512, dict(exact=True, warmup=True)), ("rho", 16, dict(exact=True, warmup=False)),
+             ("rho", 64, dict(exact=True, warmup=False, nearfar=False))]
     for pol, par, kw in cases:
         d, st, tr, ext = h.run(g.source, pol, par, trace_cap=1 << 16, ext_counts=True, snapshot=True, **kw)
         d = P.dist_to_u64(d)
