@@ -97,12 +97,14 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t *d_offsets, const in
                                  and every frontier vertex relaxes with its key at Extract (reading R8).
                                  Default ("live"): light vertices relax while Extract is still running,
                                  fewer barriers; distances are identical, round counts may differ.     */
+#define SSSP_RUN_NO_FUSE 32u    /* live rounds on sparse graphs (m < 20 n): do not extract a vertex
+                                   improved to <= theta on the spot (DESIGN.md fusion) */
 #define SSSP_RUN_NO_NEARFAR 16u /* rho: list all of Q in the queue array every round instead of only
                                    its near part (keys <= split; DESIGN.md §5 near/far)              */
 
 typedef struct {
     uint32_t flags;
-    uint32_t reserved;
+    uint32_t fuse_budget;   /* fusion: vertices a warp may extract on the spot per round (0 = default) */
     uint64_t seed;          /* rho sampling: counter-based generator seed (reading R6)      */
     int64_t max_rounds;     /* 0 = default (4n + 64); exceeded -> SSSP_ERR_ROUNDS                     */
     void *d_trace;          /* nullable device sssp_round[trace_cap]; filled when SSSP_RUN_STATS      */

@@ -32,6 +32,7 @@ POLICIES = {"rho": SSSP_RHO, "delta": SSSP_DELTA, "bellman_ford": SSSP_BELLMAN_F
             "dijkstra": SSSP_DIJKSTRA}
 SSSP_VALIDATE = 1
 SSSP_RUN_RHO_EXACT, SSSP_RUN_NO_WARMUP, SSSP_RUN_STATS, SSSP_RUN_SNAPSHOT, SSSP_RUN_NO_NEARFAR = 1, 2, 4, 8, 16
+SSSP_RUN_NO_FUSE = 32
 SSSP_SELECT_SAMPLED, SSSP_SELECT_EXACT = 0, 1
 
 
@@ -44,7 +45,7 @@ class SSSPError(RuntimeError):
 
 
 class sssp_run_opts(ctypes.Structure):
-    _fields_ = [("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32), ("seed", ctypes.c_uint64),
+    _fields_ = [("flags", ctypes.c_uint32), ("fuse_budget", ctypes.c_uint32), ("seed", ctypes.c_uint64),
                 ("max_rounds", ctypes.c_int64), ("d_trace", ctypes.c_void_p), ("trace_cap", ctypes.c_int64),
                 ("d_ext_count", ctypes.c_void_p)]
 
@@ -155,7 +156,8 @@ class SSSP:
         return SSSP(off, idx, w, validate=validate)
 
     def run(self, source, policy="rho", param=0, out=None, stats=False, trace_cap=0, ext_counts=False,
-            exact=False, warmup=True, seed=0, max_rounds=0, snapshot=False, nearfar=True):
+            exact=False, warmup=True, seed=0, max_rounds=0, snapshot=False, nearfar=True, fuse=True,
+            fuse_budget=0):
         """Alg. 1 from `source`; returns a uint64-valued int64 tensor of distances (INF = -1 as int64).
 
         With stats=True returns (dist, stats_dict, trace ndarray | None, ext_count tensor | None)."""
@@ -166,7 +168,8 @@ class SSSP:
         o = sssp_run_opts()
         o.flags = (SSSP_RUN_RHO_EXACT if exact else 0) | (0 if warmup else SSSP_RUN_NO_WARMUP) | \
                   (SSSP_RUN_STATS if (stats or trace_cap) else 0) | (SSSP_RUN_SNAPSHOT if snapshot else 0) | \
-                  (0 if nearfar else SSSP_RUN_NO_NEARFAR)
+                  (0 if nearfar else SSSP_RUN_NO_NEARFAR) | (0 if fuse else SSSP_RUN_NO_FUSE)
+        o.fuse_budget = fuse_budget
         o.seed = seed
         o.max_rounds = max_rounds
         trace = None

@@ -61,11 +61,17 @@ constexpr int kMinBlocks = SSSP_MIN_BLOCKS;  // CTAs per SM the register budget 
 constexpr int kArcs = SSSP_ARCS;             // arcs per lane in flight
 constexpr int kChunk = 32 * kArcs;           // arcs per heavy-chunk descriptor
 constexpr int kLight = SSSP_LIGHT;           // out-degree <= kLight: relaxed by the extracting warp
-constexpr int kSmemSamples = 4096;           // theta samples held in shared memory (else CTA-0 fallback)
+constexpr int kSmemSamples = 2048;           // theta samples held in shared memory (else CTA-0 fallback)
 constexpr int kRankSelect = 256;             // s <= this: select by rank counting
 constexpr int kWarps = kBlock / 32;
 #ifndef SSSP_NEAR_K
 #define SSSP_NEAR_K 4
+#endif
+#ifndef SSSP_L1DIST
+#define SSSP_L1DIST 1
+#endif
+#ifndef SSSP_FUSE
+#define SSSP_FUSE 256
 #endif
 #ifndef SSSP_ENT
 #define SSSP_ENT 4
@@ -73,6 +79,8 @@ constexpr int kWarps = kBlock / 32;
 constexpr int kEnt = SSSP_ENT;               // queue entries per lane per Extract step (large queues)
 constexpr int kQBuf = 256;                   // staged queue ids per warp (>= 32 * kArcs)
 constexpr int kTBuf = 32 * kEnt + 32;        // staged extracted ids per warp
+constexpr int kFBuf = 32 * kArcs + 64;       // fused vertices waiting for their relax, per warp
+constexpr int kFuseBudget = SSSP_FUSE;       // fused vertices per warp per round (0 = off)
 constexpr int kShards = 32;                  // append-list segments (+1 spill)
 constexpr int kSeg = kShards + 1;
 constexpr int kCntStride = 256;              // int32 words between counters (1 KB: distinct L2 slices)
@@ -150,6 +158,7 @@ struct RunParams {
     sssp_round* trace;
     int64_t trace_cap;
     int32_t* ext_count;
+    int32_t fuse_budget;  // fused vertices per warp per round (FUSE kernels)
 };
 
 __device__ __forceinline__ int32_t* counters_of(const RunParams& p, int slot, int list) {
@@ -200,6 +209,15 @@ __device__ __forceinline__ uint64_t globaltimer() {
 // small round is spread over the whole GPU instead of the first few CTAs.
 __device__ __forceinline__ int64_t warp_rank() { return (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x; }
 
+// Filter read of delta[v] for a relaxation: through L1 (hub targets are shared by many
+// arcs of an SM).  A stale L1 copy can only be higher than the current value (delta only
+// decreases, and every grid barrier's fence invalidates L1), so it can only cause a CAS
+// that then fails and retries with the word the CAS returned: never a lost update.
+__device__ __forceinline__ uint64_t dist_filter_ld(const uint64_t* p) {
+    if (SSSP_L1DIST) return __ldca((const unsigned long long*)p);
+    return ld_cg_u64(p);
+}
+
 __host__ __device__ constexpr bool uses_min(int pol) { return pol == SSSP_DELTA || pol == SSSP_DIJKSTRA; }
 
 // --------------------------------------------------------------------- segment prefix
@@ -242,21 +260,36 @@ struct WarpStage {
     int32_t take[kTBuf];  // ids that pass the theta test, extracted 32 at a time
     int32_t q[kQBuf];     // ids appended to the next queue
 };
+struct FuseStage {        // FUSE kernels only (kept out of the others' shared memory, which is L1)
+    uint64_t fd[kFBuf];   // fused vertices: key ...
+    int32_t fid[kFBuf];   // ... and id
+};
+
+// dynamic shared memory: per-warp stages, theta samples, select scratch [, fuse stages]
+constexpr size_t kSmemBase = (kWarps * sizeof(WarpStage) + kSmemSamples * sizeof(uint64_t) + sizeof(SelectSmem) + 15) /
+                             16 * 16;
 
 struct Acc {
     uint64_t minsucc = kInf;
     uint32_t succ = 0;
     uint32_t inserts = 0;
+    uint32_t fused = 0;        // STATS: vertices extracted by fusion
+    uint64_t fused_edges = 0;  // STATS: their arcs
 };
 
 struct Warp {  // per-warp working state (qn is warp-uniform)
     WarpStage* st;
+    FuseStage* fs;
     Sharded<int32_t> qnext;
     RoundCnt* C;
-    uint64_t split;  // near/far split: keys <= split are held in the queue array
-    int64_t qdelta;  // this lane's inserts - extractions (|Q| bookkeeping)
+    uint64_t split;       // near/far split: keys <= split are held in the queue array
+    uint64_t fuse_theta;  // live rounds: theta (a vertex outside Q improved to <= theta is
+                          // extracted on the spot, DESIGN.md §5 "fusion"); 0 = no fusion
+    int64_t qdelta;       // this lane's inserts - extractions (|Q| bookkeeping)
     int shard;
     int32_t qn;
+    int32_t fn;       // staged fused vertices (warp-uniform)
+    int32_t fbudget;  // fusions left this round (warp-uniform)
     Acc acc;
 };
 
@@ -318,30 +351,44 @@ __device__ __forceinline__ void wq_push1(Warp& W, bool pred, int32_t id) {
 }
 
 // --------------------------------------------------------------------- relax
-// WriteMin(delta[v], c) on the packed word, given a prior read `w`.
-// Returns true iff this lane inserted v into Q (its flag bit was set) and must append it.
-template <int POL, bool STATS>
-__device__ __forceinline__ bool write_min(uint64_t* dist, int32_t v, uint64_t c, uint64_t w, Warp& W) {
+// Outcome of a relaxation slot.
+enum { kNone = 0, kAppend = 1, kFused = 2 };
+
+// The word a successful WriteMin of c over word w writes: c with the flag cleared (v is
+// in Q), or - when fusing - c with the flag still set (v was outside Q and is extracted
+// on the spot by this warp, so it never enters Q).
+__device__ __forceinline__ bool fuses(bool fuse, uint64_t w, uint64_t c, const Warp& W) {
+    return fuse && (w & kTop) && c <= W.fuse_theta;
+}
+
+// WriteMin(delta[v], c) on the packed word, given a prior read `w`: CAS retries.
+template <int POL, bool STATS, bool FUSE>
+__device__ __forceinline__ int write_min(uint64_t* dist, int32_t v, uint64_t c, uint64_t w, bool fuse, Warp& W) {
     while ((w & kVal) > c) {
-        const uint64_t old = atomicCAS((unsigned long long*)(dist + v), (unsigned long long)w, (unsigned long long)c);
+        const bool f = fuses(fuse, w, c, W);
+        const uint64_t old = atomicCAS((unsigned long long*)(dist + v), (unsigned long long)w,
+                                       (unsigned long long)(f ? (c | kTop) : c));
         if (old == w) {
             if (STATS) W.acc.succ++;
+            if (f) return kFused;
             if (uses_min(POL)) W.acc.minsucc = c < W.acc.minsucc ? c : W.acc.minsucc;
-            return admit<STATS>(w, c, W);
+            return admit<STATS>(w, c, W) ? kAppend : kNone;
         }
         w = old;
     }
-    return false;
+    return kNone;
 }
 
 // Relax kArcs arcs per lane (v < 0 = empty slot): filter loads, WriteMins, stage the
 // inserted ids (Alg. 1 lines 5-6).
-template <int POL, bool STATS>
+template <int POL, bool STATS, bool FUSE>
 __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&v)[kArcs], const uint64_t (&c)[kArcs],
                                             Warp& W) {
     uint64_t cur[kArcs];
 #pragma unroll
-    for (int t = 0; t < kArcs; t++) cur[t] = v[t] >= 0 ? ld_cg_u64(p.dist + v[t]) : 0ull;
+    for (int t = 0; t < kArcs; t++) cur[t] = v[t] >= 0 ? dist_filter_ld(p.dist + v[t]) : 0ull;
+    // room for a full step of fusions and budget left (warp-uniform)
+    const bool fuse = FUSE && W.fuse_theta != 0 && W.fbudget > 0 && W.fn <= kFBuf - 32 * kArcs;
     // first CAS attempt of every slot issued back to back (one round trip, not kArcs),
     // then the rare retries
     uint64_t old[kArcs];
@@ -349,39 +396,58 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
     for (int t = 0; t < kArcs; t++)
         old[t] = (v[t] >= 0 && (cur[t] & kVal) > c[t])
                      ? atomicCAS((unsigned long long*)(p.dist + v[t]), (unsigned long long)cur[t],
-                                 (unsigned long long)c[t])
+                                 (unsigned long long)(fuses(fuse, cur[t], c[t], W) ? (c[t] | kTop) : c[t]))
                      : cur[t] + 1;  // "no attempt" marker: != cur[t]
-    int32_t cnt = 0;
-    bool app[kArcs];
+    int32_t cnt = 0, fcnt = 0;
+    int out[kArcs];
 #pragma unroll
     for (int t = 0; t < kArcs; t++) {
+        out[t] = kNone;
         if (v[t] >= 0 && (cur[t] & kVal) > c[t]) {
             if (old[t] == cur[t]) {
                 if (STATS) W.acc.succ++;
-                if (uses_min(POL)) W.acc.minsucc = c[t] < W.acc.minsucc ? c[t] : W.acc.minsucc;
-                app[t] = admit<STATS>(cur[t], c[t], W);
+                if (fuses(fuse, cur[t], c[t], W)) {
+                    out[t] = kFused;
+                } else {
+                    if (uses_min(POL)) W.acc.minsucc = c[t] < W.acc.minsucc ? c[t] : W.acc.minsucc;
+                    out[t] = admit<STATS>(cur[t], c[t], W) ? kAppend : kNone;
+                }
             } else {
-                app[t] = write_min<POL, STATS>(p.dist, v[t], c[t], old[t], W);
+                out[t] = write_min<POL, STATS, FUSE>(p.dist, v[t], c[t], old[t], fuse, W);
             }
-        } else {
-            app[t] = false;
         }
-        cnt += app[t];
+        cnt += out[t] == kAppend;
+        fcnt += out[t] == kFused;
     }
-    if (!__any_sync(kFull, cnt != 0)) return;
-    const int32_t incl = warp_incl_scan(cnt);
-    const int32_t tot = __shfl_sync(kFull, incl, 31);
-    if (W.qn + tot > kQBuf) wq_flush(W);
-    int32_t pos = W.qn + incl - cnt;
+    if (__any_sync(kFull, cnt != 0)) {
+        const int32_t incl = warp_incl_scan(cnt);
+        const int32_t tot = __shfl_sync(kFull, incl, 31);
+        if (W.qn + tot > kQBuf) wq_flush(W);
+        int32_t pos = W.qn + incl - cnt;
 #pragma unroll
-    for (int t = 0; t < kArcs; t++)
-        if (app[t]) W.st->q[pos++] = v[t];
-    W.qn += tot;
+        for (int t = 0; t < kArcs; t++)
+            if (out[t] == kAppend) W.st->q[pos++] = v[t];
+        W.qn += tot;
+    }
+    if (FUSE && fuse && __any_sync(kFull, fcnt != 0)) {
+        const int32_t incl = warp_incl_scan(fcnt);
+        const int32_t tot = __shfl_sync(kFull, incl, 31);
+        int32_t pos = W.fn + incl - fcnt;
+#pragma unroll
+        for (int t = 0; t < kArcs; t++)
+            if (out[t] == kFused) {
+                W.fs->fid[pos] = v[t];
+                W.fs->fd[pos] = c[t];
+                pos++;
+            }
+        W.fn += tot;
+        W.fbudget -= tot;
+    }
 }
 
 // One chunk: arcs [beg, beg+len) of a vertex with key d, len <= kChunk.  Lane-strided
 // so every load instruction of the warp reads 128 contiguous bytes.
-template <int POL, bool STATS>
+template <int POL, bool STATS, bool FUSE>
 __device__ __forceinline__ void relax_chunk(const RunParams& p, uint64_t d, int32_t beg, int32_t len, Warp& W) {
     const int lane = lane_id();
     int32_t v[kArcs];
@@ -392,12 +458,12 @@ __device__ __forceinline__ void relax_chunk(const RunParams& p, uint64_t d, int3
         v[t] = k < len ? ld_stream_i32(p.idx + beg + k) : -1;
         c[t] = d + (k < len ? ld_stream_u32(p.w + beg + k) : 0u);
     }
-    relax_slots<POL, STATS>(p, v, c, W);
+    relax_slots<POL, STATS, FUSE>(p, v, c, W);
 }
 
 // Up to 32 vertices, one per lane (deg = 0 for none): the warp walks their
 // concatenated arc lists; arc e belongs to the largest lane o with excl[o] <= e.
-template <int POL, bool STATS>
+template <int POL, bool STATS, bool FUSE>
 __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, int32_t beg, int32_t deg, Warp& W) {
     const int lane = lane_id();
     const int32_t incl = warp_incl_scan(deg);
@@ -422,7 +488,39 @@ __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, i
             v[t] = ok ? ld_stream_i32(p.idx + rb + e) : -1;
             c[t] = od + (ok ? ld_stream_u32(p.w + rb + e) : 0u);
         }
-        relax_slots<POL, STATS>(p, v, c, W);
+        relax_slots<POL, STATS, FUSE>(p, v, c, W);
+    }
+}
+
+// Relax the fused vertices (already deleted from / never entered Q, key known), 32 at a
+// time from the top of the warp's stack; their relaxations may fuse more.
+template <int POL, bool STATS, bool FUSE>
+__device__ __forceinline__ void fuse_drain(const RunParams& p, Warp& W) {
+    if (!FUSE) return;
+    const int lane = lane_id();
+    while (W.fn > 0) {
+        const int32_t cnt = W.fn < 32 ? W.fn : 32;
+        __syncwarp();
+        int32_t id = -1;
+        uint64_t d = 0;
+        if (lane < cnt) {
+            id = W.fs->fid[W.fn - cnt + lane];
+            d = W.fs->fd[W.fn - cnt + lane];
+        }
+        __syncwarp();
+        W.fn -= cnt;
+        int32_t beg = 0, deg = 0;
+        if (id >= 0) {
+            beg = __ldg(p.off + id);
+            deg = __ldg(p.off + id + 1) - beg;
+            if (p.ext_count) atomicAdd(p.ext_count + id, 1);
+            if (STATS) {
+                W.acc.fused++;  // counted as inserted and extracted (the |Q| identity holds)
+                W.acc.inserts++;
+                W.acc.fused_edges += (uint64_t)deg;
+            }
+        }
+        relax_vertices<POL, STATS, FUSE>(p, d, beg, deg, W);
     }
 }
 
@@ -467,7 +565,7 @@ __device__ __forceinline__ void emit_chunks(const Sharded<Desc>& CL, int shard, 
 //  batch: 32 staged ids at a time are deleted from Q (atomicOr, which returns the exact
 //         key they relax with), their CSR rows read, heavy ones cut into chunks and the
 //         light ones relaxed by the warp at once (live) or listed (snapshot).
-template <int POL, bool STATS>
+template <int POL, bool STATS, bool FUSE>
 __device__ __forceinline__ void take_batch(const RunParams& p, int32_t cnt, const Sharded<Desc>& CL, bool snap, Warp& W,
                                            uint64_t& fs, uint64_t& edges) {
     const int lane = lane_id();
@@ -497,11 +595,11 @@ __device__ __forceinline__ void take_batch(const RunParams& p, int32_t cnt, cons
         const int32_t ls = warp_append_slot(light, &W.C->nlight);
         if (light) st_desc(p.light + ls, d, beg, deg);
     } else if (__any_sync(kFull, light)) {
-        relax_vertices<POL, STATS>(p, d, beg, light ? deg : 0, W);
+        relax_vertices<POL, STATS, FUSE>(p, d, beg, light ? deg : 0, W);
     }
 }
 
-template <int POL, bool STATS>
+template <int POL, bool STATS, bool FUSE>
 __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_t>& QC, const int64_t* qpref,
                                         const Sharded<Desc>& CL, uint64_t theta, bool snap, uint64_t& minrem, Warp& W) {
     const int lane = lane_id();
@@ -547,7 +645,7 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
                 __syncwarp();
                 W.st->take[lane] = x;
             }
-            take_batch<POL, STATS>(p, 32, CL, snap, W, fs, edges);
+            take_batch<POL, STATS, FUSE>(p, 32, CL, snap, W, fs, edges);
             done += 32;
         }
         if (done) {  // keep the remainder (< 32) at the front
@@ -560,7 +658,8 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
             tn -= done;
         }
     }
-    if (tn) take_batch<POL, STATS>(p, tn, CL, snap, W, fs, edges);
+    if (tn) take_batch<POL, STATS, FUSE>(p, tn, CL, snap, W, fs, edges);
+    fuse_drain<POL, STATS, FUSE>(p, W);
     if (STATS) {
         fs = warp_sum(fs);
         edges = warp_sum(edges);
@@ -570,7 +669,7 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
 }
 
 // --------------------------------------------------------------------- phase B
-template <int POL, bool STATS>
+template <int POL, bool STATS, bool FUSE>
 __device__ __forceinline__ void phase_b(const RunParams& p, const Sharded<Desc>& CL, const int64_t* cpref, int32_t nl,
                                         Warp& W) {
     const int lane = lane_id();
@@ -597,17 +696,19 @@ __device__ __forceinline__ void phase_b(const RunParams& p, const Sharded<Desc>&
                 e.beg = 0;
                 e.len = 0;
             }
-            relax_vertices<POL, STATS>(p, e.d, e.beg, e.len, W);
+            relax_vertices<POL, STATS, FUSE>(p, e.d, e.beg, e.len, W);
             if (item + nwarps >= nb && item + nwarps < total) nxt = chunk_at(item + nwarps - nb);
         } else {
             const Desc e = nxt;
             if (item + nwarps < total) nxt = chunk_at(item + nwarps - nb);  // prefetch
-            relax_chunk<POL, STATS>(p, e.d, e.beg, e.len, W);
+            relax_chunk<POL, STATS, FUSE>(p, e.d, e.beg, e.len, W);
+            if (FUSE && W.fn > kFBuf - 32 * kArcs) fuse_drain<POL, STATS, FUSE>(p, W);
         }
     }
+    fuse_drain<POL, STATS, FUSE>(p, W);
 }
 
-template <int POL, bool STATS>
+template <int POL, bool STATS, bool FUSE>
 __device__ __forceinline__ void flush_acc(const RunParams& p, int64_t r, Warp& W) {
     wq_flush(W);
     const int64_t dq = warp_sum(W.qdelta);
@@ -615,12 +716,17 @@ __device__ __forceinline__ void flush_acc(const RunParams& p, int64_t r, Warp& W
                                         (unsigned long long)dq);
     W.qdelta = 0;
     if (STATS) {
-        const uint32_t s = warp_sum(W.acc.succ), ins = warp_sum(W.acc.inserts);
+        const uint32_t s = warp_sum(W.acc.succ), ins = warp_sum(W.acc.inserts), fu = warp_sum(W.acc.fused);
+        const uint64_t fe = warp_sum(W.acc.fused_edges);
         if (lane_id() == 0 && s) atomicAdd(&W.C->succ, (unsigned long long)s);
         if (lane_id() == 0 && ins) atomicAdd(&W.C->inserts, (unsigned long long)ins);
+        if (lane_id() == 0 && fu) atomicAdd(&W.C->fsize, (unsigned long long)fu);
+        if (lane_id() == 0 && fe) atomicAdd(&W.C->edges, (unsigned long long)fe);
     }
     W.acc.succ = 0;
     W.acc.inserts = 0;
+    W.acc.fused = 0;
+    W.acc.fused_edges = 0;
 }
 
 // --------------------------------------------------------------------- ExtDist for rho
@@ -727,12 +833,13 @@ __device__ uint64_t far_quantile(const RunParams& p, uint64_t split, int64_t far
 }
 
 // --------------------------------------------------------------------- the round loop
-template <int POL, bool STATS>
+template <int POL, bool STATS, bool FUSE>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpStage* stage = (WarpStage*)smem_raw;                                // [kWarps]
     uint64_t* s_keys = (uint64_t*)(smem_raw + kWarps * sizeof(WarpStage));  // [kSmemSamples]
     SelectSmem& sm = *(SelectSmem*)(s_keys + kSmemSamples);
+    FuseStage* fstage = (FuseStage*)(smem_raw + kSmemBase);                  // [kWarps], FUSE only
     __shared__ int64_t qpref[kSeg + 1];  // segment prefix of Q_r's near part
     __shared__ int64_t cpref[kSeg + 1];  // segment prefix of the round's chunk list
     __shared__ uint64_t bc_u[3];         // min_Q (Delta / Dijkstra), CTA-0 theta, CTA-0 split
@@ -742,8 +849,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     Ctrl* ctrl = p.ctrl;
     Warp W;
     W.st = stage + (threadIdx.x >> 5);
+    W.fs = fstage + (threadIdx.x >> 5);
     W.shard = (int)(warp_rank() % kShards);
     W.qn = 0;
+    W.fn = 0;
     W.qdelta = 0;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
@@ -936,12 +1045,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             }
         }
         W.split = split;
+        W.fuse_theta = snap ? 0 : theta;  // fusion only in live rounds
+        W.fbudget = p.fuse_budget;
         if (STATS && gtid == 0) t1 = globaltimer();
 
         // ---- phase A: Extract(theta) (+ light relax in live mode)
         uint64_t minrem = kInf;
-        phase_a<POL, STATS>(p, QC, qpref, CL, theta, snap, minrem, W);
-        flush_acc<POL, STATS>(p, r, W);
+        phase_a<POL, STATS, FUSE>(p, QC, qpref, CL, theta, snap, minrem, W);
+        flush_acc<POL, STATS, FUSE>(p, r, W);
         grid_sync(nullptr);
         if (STATS && gtid == 0) t2 = globaltimer();
         // ---- phase B: heavy chunks (+ light list in snapshot mode)
@@ -950,7 +1061,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         __syncthreads();
         const int32_t nl = bc_nl;
         const bool phase_b_work = cpref[kSeg] + nl > 0;
-        if (phase_b_work) phase_b<POL, STATS>(p, CL, cpref, nl, W);
+        if (phase_b_work) phase_b<POL, STATS, FUSE>(p, CL, cpref, nl, W);
         if (uses_min(POL)) {  // this CTA's min over kept ids and successful WriteMins
             uint64_t mn = warp_min_u64(minrem < W.acc.minsucc ? minrem : W.acc.minsucc);
             if (lane_id() == 0) red[threadIdx.x >> 5] = mn;
@@ -962,7 +1073,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             W.acc.minsucc = kInf;
         }
         if (phase_b_work) {
-            flush_acc<POL, STATS>(p, r, W);
+            flush_acc<POL, STATS, FUSE>(p, r, W);
             grid_sync(nullptr);
         } else if (uses_min(POL) || STATS) {
             grid_sync(nullptr);
@@ -1086,12 +1197,12 @@ Layout carve(void* base, int32_t n, int64_t m) {
 
 typedef void (*KernelFn)(RunParams);
 
-constexpr size_t kSmemBytes = kWarps * sizeof(WarpStage) + kSmemSamples * sizeof(uint64_t) + sizeof(SelectSmem);
+constexpr size_t smem_bytes(bool fuse) { return kSmemBase + (fuse ? kWarps * sizeof(FuseStage) : 0); }
 
 template <int POL>
-KernelFn kernel_for_pol(bool stats, bool snap) {
-    (void)snap;  // snapshot rounds are a runtime flag
-    return stats ? sssp_round_loop<POL, true> : sssp_round_loop<POL, false>;
+KernelFn kernel_for_pol(bool stats, bool fuse) {
+    if (fuse) return stats ? sssp_round_loop<POL, true, true> : sssp_round_loop<POL, false, true>;
+    return stats ? sssp_round_loop<POL, true, false> : sssp_round_loop<POL, false, false>;
 }
 
 KernelFn kernel_for(int pol, bool stats, bool snap) {
@@ -1173,10 +1284,10 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
             for (int sn = 0; sn < 2; sn++) {
                 int per_sm = 0;
                 e = cudaFuncSetAttribute((const void*)kernel_for(pol, st, sn),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(sn));
                 if (e == cudaSuccess)
                     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kernel_for(pol, st, sn),
-                                                                      kBlock, kSmemBytes);
+                                                                      kBlock, smem_bytes(sn));
                 if (e != cudaSuccess || per_sm < 1) {
                     delete h;
                     return e != cudaSuccess ? cuda_error(e, "occupancy query")
@@ -1231,7 +1342,10 @@ sssp_status sssp_run_ex(sssp_handle* h, int32_t source, sssp_policy policy, uint
     memset(&o, 0, sizeof(o));
     if (opts) o = *opts;
     const bool st = (o.flags & SSSP_RUN_STATS) != 0;
-    const bool sn = (o.flags & SSSP_RUN_SNAPSHOT) != 0;
+    // fusion ("local relaxation within theta") in live rounds of sparse graphs:
+    // the paper applies it when the average degree is below 20
+    const bool fu = !(o.flags & (SSSP_RUN_SNAPSHOT | SSSP_RUN_NO_FUSE)) && policy != SSSP_DIJKSTRA &&
+                    h->m < 20 * (int64_t)h->n;
     RunParams p = h->base;
     p.dist = d_dist_out;
     p.source = source;
@@ -1242,11 +1356,12 @@ sssp_status sssp_run_ex(sssp_handle* h, int32_t source, sssp_policy policy, uint
     p.trace = st ? (sssp_round*)o.d_trace : nullptr;
     p.trace_cap = o.trace_cap;
     p.ext_count = o.d_ext_count;
-    KernelFn k = kernel_for(policy, st, sn);
-    const int grid = h->grid[policy][st][sn];
+    p.fuse_budget = o.fuse_budget ? (int32_t)o.fuse_budget : kFuseBudget;
+    KernelFn k = kernel_for(policy, st, fu);
+    const int grid = h->grid[policy][st][fu];
     void* args[] = {&p};
     cudaEventRecord(h->ev[0], h->stream);
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kBlock), args, kSmemBytes, h->stream);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kBlock), args, smem_bytes(fu), h->stream);
     if (e != cudaSuccess) return cuda_error(e, "round-loop launch");
     cudaEventRecord(h->ev[1], h->stream);
     e = cudaMemcpyAsync(&h->h_ctrl->status, &h->ctrl->status, sizeof(Ctrl) - offsetof(Ctrl, status),
