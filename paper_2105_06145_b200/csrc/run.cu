@@ -46,10 +46,10 @@ namespace sssp {
 #define SSSP_MIN_BLOCKS 1
 #endif
 #ifndef SSSP_BLOCK
-#define SSSP_BLOCK 768
+#define SSSP_BLOCK 1024
 #endif
 #ifndef SSSP_ARCS
-#define SSSP_ARCS 8
+#define SSSP_ARCS 4
 #endif
 #ifndef SSSP_LIGHT
 #define SSSP_LIGHT 128
@@ -74,7 +74,7 @@ constexpr int kWarps = kBlock / 32;
 #define SSSP_FUSE 256
 #endif
 #ifndef SSSP_ENT
-#define SSSP_ENT 4
+#define SSSP_ENT 2
 #endif
 constexpr int kEnt = SSSP_ENT;               // queue entries per lane per Extract step (large queues)
 constexpr int kQBuf = 256;                   // staged queue ids per warp (>= 32 * kArcs)
