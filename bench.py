@@ -132,6 +132,40 @@ def make_graph(name):
     return gen.make(name)
 
 
+def replica_source(g, rank):
+    """Source of a replica: rank 0 runs the workload's source, rank r > 0 a seeded random
+    non-isolated vertex (independent single-source problems: no data-path collective)."""
+    import numpy as np
+
+    if rank == 0:
+        return int(g.source)
+    rs = np.random.default_rng(1000 + rank)
+    deg = g.degrees
+    while True:
+        v = int(rs.integers(0, g.n))
+        if deg[v] > 0:
+            return v
+
+
+def max_over_ranks(x, ws, dist=None, device=None):
+    """Max of a per-rank float over the job (the timing rule: the slowest rank decides)."""
+    if ws <= 1:
+        return float(x)
+    import torch
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def workload_config(args, g, source, param, ws):
+    """The `config` object, identical in both arms (ours and --impl reference)."""
+    return {"workload": f"{args.config}: {CONFIG_DESC.get(args.config, args.config)}",
+            "n": g.n, "m": g.m, "source": source, "policy": args.policy, "param": param,
+            "parallelism": f"replicas x{ws} (independent sources, no collective)",
+            "l2": "GPU arm: L2 flushed between timed steps (256 MiB write); reference arm: host CPU"}
+
+
 def emit(obj):
     print(json.dumps(obj), flush=True)
 
@@ -152,6 +186,7 @@ def run_reference(args):
     if rank != 0:
         return  # rank 0 alone runs the CPU oracle arm
     g = make_graph(args.config)
+    param = DEFAULT_PARAM[args.policy] if args.param is None else args.param
     budget = min(g.m, 20_000_000)
     for _ in range(args.warmup):
         cpu_oracle_sample(g, g.source, budget)
@@ -168,8 +203,7 @@ def run_reference(args):
           "unit": "GTEPS", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
           "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
           "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-          "config": {"workload": f"{args.config}: {CONFIG_DESC.get(args.config, args.config)}",
-                     "n": g.n, "m": g.m, "source": g.source},
+          "config": workload_config(args, g, g.source, param, ws),
           "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": 1, "kind": "oracle", "sample": sample},
           "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
@@ -197,16 +231,7 @@ def main():
     t_gen = time.perf_counter()
     g = make_graph(args.config)
     t_gen = time.perf_counter() - t_gen
-    # replicas: rank 0 uses the workload source; other ranks a seeded random non-isolated vertex
-    source = g.source
-    if rank > 0:
-        rs = np.random.default_rng(1000 + rank)
-        deg = g.degrees
-        while True:
-            v = int(rs.integers(0, g.n))
-            if deg[v] > 0:
-                source = v
-                break
+    source = replica_source(g, rank)
     h = P.SSSP.from_graph(g, device=dev)
     stream = h.stream
     out = torch.empty(g.n, dtype=torch.int64, device=dev)
@@ -238,11 +263,7 @@ def main():
         kern_ms.append(h.last_stats["kernel_ms"])
         rounds.append(h.last_stats["rounds"])
     barrier()
-    total_ms = sum(step_ms)
-    if ws > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(step_ms), ws, dist, dev)
     clocks = sampler.stop()
     ms_per_step = total_ms / args.steps
     value = ws * g.m / (ms_per_step * 1e-3) / 1e9
@@ -254,11 +275,7 @@ def main():
     t0 = time.perf_counter()
     for k in range(args.steps):
         h.run_host(source, args.policy, param, host)
-    e2e_s = time.perf_counter() - t0
-    if ws > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(time.perf_counter() - t0, ws, dist, dev)
     e2e = ws * g.m * args.steps / e2e_s / 1e9
 
     # algorithmic bytes from a counters run of the same workload
@@ -285,12 +302,10 @@ def main():
     emit({"metric": "SSSP GTEPS (m / device time per source)", "value": value, "unit": "GTEPS", "n_gpus": ws,
           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
           "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-          "config": {"workload": f"{args.config}: {CONFIG_DESC.get(args.config, args.config)}",
-                     "n": g.n, "m": g.m, "source": source, "policy": args.policy, "param": param,
-                     "parallelism": f"replicas x{ws} (independent sources, no collective)",
-                     "l2": "flushed between timed steps (256 MiB write)" if flush is not None else "not flushed",
-                     "rounds_median": statistics.median(rounds), "kernel_ms_mean": kern_avg,
-                     "grid": [st["grid_blocks"], st["block_threads"]], "gen_s": round(t_gen, 1)},
+          "config": workload_config(args, g, g.source, param, ws),
+          "run": {"source_this_rank": source, "l2_flushed": flush is not None,
+                  "rounds_median": statistics.median(rounds), "kernel_ms_mean": kern_avg,
+                  "grid": [st["grid_blocks"], st["block_threads"]], "gen_s": round(t_gen, 1)},
           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                        "traffic": traffic, "peak_source": peak_src,
                        "frac_of_8TBps": achieved / 8000.0,
