@@ -17,9 +17,9 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 INF = np.uint64(0xFFFFFFFFFFFFFFFF)
 INF_INT = 0xFFFFFFFFFFFFFFFF
 
-RHO, DELTA, BF, DIJKSTRA = 0, 1, 2, 3
+RHO, DELTA, BF, DIJKSTRA, DELTA_STEPPING = 0, 1, 2, 3, 4
 RHO_EXACT, RHO_WARMUP = 1, 2
-POLICIES = {"rho": RHO, "delta": DELTA, "bellman_ford": BF, "dijkstra": DIJKSTRA}
+POLICIES = {"rho": RHO, "delta": DELTA, "bellman_ford": BF, "dijkstra": DIJKSTRA, "delta_stepping": DELTA_STEPPING}
 
 ROUND_DTYPE = np.dtype([("qsize", "<i8"), ("fsize", "<i8"), ("edges", "<i8"), ("inserts", "<i8"),
                         ("succ", "<i8"), ("theta", "<u8"), ("pad0", "<i8"), ("pad1", "<i8")])

@@ -303,6 +303,20 @@ int64_t oracle_stepping_sim(int32_t n, const int32_t *off, const int32_t *idx, c
             uint64_t b = (minq / D + (minq % D != 0)) * D; /* ceil(min_Q / D) * D; min_Q < 2^63 */
             theta = a > b ? a : b;
             theta_prev = theta;
+        } else if (policy == ORACLE_DELTA_STEPPING) {
+            /* Delta-stepping with FinishCheck (Table tab:framework P:791): theta = i*Delta,
+             * and "if no new delta[v] < i*Delta, i <- i+1": while Q still holds a key <= i*Delta the
+             * same bucket is extracted again (a Bellman-Ford substep, reading R19); otherwise i
+             * advances, skipping empty buckets as for Delta* (reading R2). */
+            uint64_t D = param;
+            if (round > 1 && minq <= theta_prev) {
+                theta = theta_prev;
+            } else {
+                uint64_t a = sat_add(theta_prev, D);
+                uint64_t b = (minq / D + (minq % D != 0)) * D;
+                theta = a > b ? a : b;
+            }
+            theta_prev = theta;
         } else { /* RHO */
             uint64_t rho = param;
             if ((flags & ORACLE_RHO_WARMUP) && (uint64_t)q > rho && warm_rounds < 2) {

@@ -61,7 +61,7 @@ int oracle_certify(int32_t n, const int32_t *off, const int32_t *idx, const uint
                    const uint64_t *d, int64_t *bad);
 
 /* Policies of Table tab:framework. */
-enum { ORACLE_RHO = 0, ORACLE_DELTA = 1, ORACLE_BF = 2, ORACLE_DIJKSTRA = 3 };
+enum { ORACLE_RHO = 0, ORACLE_DELTA = 1, ORACLE_BF = 2, ORACLE_DIJKSTRA = 3, ORACLE_DELTA_STEPPING = 4 };
 /* flags */
 enum { ORACLE_RHO_EXACT = 1, ORACLE_RHO_WARMUP = 2 };
 
@@ -86,6 +86,8 @@ typedef struct {
  *              |Q| <= rho -> +inf; warm-up rho/10 in the first two
  *              rounds with |Q| > rho (reading R7).
  *   DIJKSTRA:  theta = min_Q key
+ *   DELTA_STEPPING: theta_i = i*Delta with FinishCheck: the same theta again while
+ *              min_Q <= theta (substeps), else as DELTA        (reading R19)
  * Writes distances, per-round trace (up to trace_cap rows), and optional
  * per-vertex extraction counts.  Returns rounds, or -1 if max_rounds exceeded. */
 int64_t oracle_stepping_sim(int32_t n, const int32_t *off, const int32_t *idx, const uint32_t *w, int32_t s,

@@ -323,6 +323,34 @@ def test_sim_delta_huge_is_bf():
     assert len(a) == len(b) and (a["fsize"] == b["fsize"]).all()
 
 
+def test_sim_delta_stepping_pins():
+    """Delta-stepping with FinishCheck (Table; reading R19).
+
+    - Distances equal Dijkstra's on random directed and undirected graphs.
+    - Delta <= min weight: bucket i holds exactly the vertices at distance i*Delta-ish, so
+      every reached vertex is extracted exactly once and the rounds are the distinct
+      finite distances (Dijkstra by distance classes).
+    - Delta >= n*L: one bucket, refilled by Bellman-Ford substeps, so the trace equals BF.
+    """
+    for g in rng_graphs(40, seed0=77, nmax=400):
+        want = oracle.dijkstra(g)
+        for D in (1, 7, 1000, 1 << 40):
+            d, tr, ext = oracle.stepping_sim(g, "delta_stepping", D, ext_counts=True)
+            assert np.array_equal(d, want), (g.name, D)
+    for name in ("grid64", "rmat12"):
+        g = gen.make(name)
+        want, hops = oracle.dijkstra(g, with_hops=True)
+        d, tr, ext = oracle.stepping_sim(g, "delta_stepping", 1, ext_counts=True)
+        fin = want != oracle.INF
+        assert np.array_equal(d, want)
+        assert (ext[fin] == 1).all()
+        assert len(tr) == len(np.unique(want[fin]))
+        _, a, _ = oracle.stepping_sim(g, "delta_stepping", g.n * (1 << 18))
+        _, b, _ = oracle.stepping_sim(g, "bellman_ford")
+        assert len(a) == len(b) and (a["fsize"] == b["fsize"]).all()
+        assert len(b) == int(hops.max()) + 1
+
+
 # ----------------------------------------------------------------------------- selection pins
 def test_select_sampled_rank_bound():
     """App. cpam: with c = 10 the sampled theta's rank lies within a constant
