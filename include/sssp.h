@@ -59,7 +59,10 @@ typedef enum {
     SSSP_DELTA = 1,        /* Delta*: theta_i = i*Delta, no FinishCheck;
                               param = Delta >= 1; empty steps skipped (reading R2)        */
     SSSP_BELLMAN_FORD = 2, /* theta = +inf; param ignored                            */
-    SSSP_DIJKSTRA = 3      /* theta = min_{v in Q} delta[v]; param ignored        */
+    SSSP_DIJKSTRA = 3,     /* theta = min_{v in Q} delta[v]; param ignored        */
+    SSSP_DELTA_STEPPING = 4 /* theta_i = i*Delta WITH FinishCheck: the bucket is extracted again while
+                              Q holds a key <= i*Delta (reading R19);
+                              param = Delta >= 1                                                    */
 } sssp_policy;
 
 typedef void *sssp_stream_t; /* a cudaStream_t */

@@ -27,9 +27,9 @@ _lib = ctypes.CDLL(LIB_PATH)
 INF = 0xFFFFFFFFFFFFFFFF
 SSSP_OK, SSSP_ERR_INVALID, SSSP_ERR_INVALID_GRAPH, SSSP_ERR_RANGE = 0, -1, -2, -3
 SSSP_ERR_CAPACITY, SSSP_ERR_CUDA, SSSP_ERR_ROUNDS, SSSP_ERR_DEVICE = -4, -5, -6, -7
-SSSP_RHO, SSSP_DELTA, SSSP_BELLMAN_FORD, SSSP_DIJKSTRA = 0, 1, 2, 3
+SSSP_RHO, SSSP_DELTA, SSSP_BELLMAN_FORD, SSSP_DIJKSTRA, SSSP_DELTA_STEPPING = 0, 1, 2, 3, 4
 POLICIES = {"rho": SSSP_RHO, "delta": SSSP_DELTA, "bellman_ford": SSSP_BELLMAN_FORD, "bf": SSSP_BELLMAN_FORD,
-            "dijkstra": SSSP_DIJKSTRA}
+            "dijkstra": SSSP_DIJKSTRA, "delta_stepping": SSSP_DELTA_STEPPING}
 SSSP_VALIDATE = 1
 SSSP_RUN_RHO_EXACT, SSSP_RUN_NO_WARMUP, SSSP_RUN_STATS, SSSP_RUN_SNAPSHOT, SSSP_RUN_NO_NEARFAR = 1, 2, 4, 8, 16
 SSSP_RUN_NO_FUSE = 32

@@ -85,6 +85,7 @@ constexpr int kShards = 32;                  // append-list segments (+1 spill)
 constexpr int kSeg = kShards + 1;
 constexpr int kCntStride = 256;              // int32 words between counters (1 KB: distinct L2 slices)
 constexpr int kMaxCtas = 4096;
+constexpr int kPolicies = 5;
 constexpr int kNearK = SSSP_NEAR_K;          // near queue target: ~kNearK rounds of extraction
 constexpr int kFarSamples = 1024;            // vertices probed to place a new near/far split
 static_assert(32 * kArcs <= kQBuf, "one relax step must fit the stage");
@@ -218,7 +219,9 @@ __device__ __forceinline__ uint64_t dist_filter_ld(const uint64_t* p) {
     return ld_cg_u64(p);
 }
 
-__host__ __device__ constexpr bool uses_min(int pol) { return pol == SSSP_DELTA || pol == SSSP_DIJKSTRA; }
+__host__ __device__ constexpr bool uses_min(int pol) {
+    return pol == SSSP_DELTA || pol == SSSP_DIJKSTRA || pol == SSSP_DELTA_STEPPING;
+}
 
 // --------------------------------------------------------------------- segment prefix
 // Exclusive prefix of a sharded list's segment counts, in shared memory (pref[kSeg] =
@@ -929,7 +932,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         bool snap = (p.flags & SSSP_RUN_SNAPSHOT) != 0;
         if (POL == SSSP_BELLMAN_FORD) {
             theta = kInf;
-        } else if (POL == SSSP_DIJKSTRA || POL == SSSP_DELTA) {
+        } else if (POL == SSSP_DIJKSTRA || POL == SSSP_DELTA || POL == SSSP_DELTA_STEPPING) {
             // min_Q delta = min over the per-CTA minima of the previous round
             if (threadIdx.x < 32) {
                 const uint64_t* cm = p.cta_min + ((r + 2) % 3) * kMaxCtas;
@@ -945,6 +948,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             const uint64_t minq = bc_u[0];  // <= min_{v in Q} delta[v] (exact in snapshot mode)
             if (POL == SSSP_DIJKSTRA) {
                 theta = minq;
+            } else if (POL == SSSP_DELTA_STEPPING && r > 1 && minq <= theta_prev) {
+                theta = theta_prev;  // FinishCheck failed: Bellman-Ford substep on the same bucket (R19)
             } else {
                 const uint64_t D = p.param;  // theta_i = i*Delta, skipping empty steps (reading R2)
                 const uint64_t x = theta_prev > kInf - D ? kInf : theta_prev + D;
@@ -1149,7 +1154,7 @@ struct sssp_handle {
     int device;
     cudaEvent_t ev[2];
     int num_sms;
-    int grid[4][2][2];
+    int grid[5][2][2];
 };
 
 namespace {
@@ -1211,6 +1216,7 @@ KernelFn kernel_for(int pol, bool stats, bool snap) {
         case SSSP_DELTA: return kernel_for_pol<SSSP_DELTA>(stats, snap);
         case SSSP_BELLMAN_FORD: return kernel_for_pol<SSSP_BELLMAN_FORD>(stats, snap);
         case SSSP_DIJKSTRA: return kernel_for_pol<SSSP_DIJKSTRA>(stats, snap);
+        case SSSP_DELTA_STEPPING: return kernel_for_pol<SSSP_DELTA_STEPPING>(stats, snap);
     }
     return nullptr;
 }
@@ -1279,7 +1285,7 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
     b.light = L.light;
     b.samples = L.samples;
     b.ctrl = L.ctrl;
-    for (int pol = 0; pol < 4; pol++)
+    for (int pol = 0; pol < kPolicies; pol++)
         for (int st = 0; st < 2; st++)
             for (int sn = 0; sn < 2; sn++) {
                 int per_sm = 0;
@@ -1333,8 +1339,8 @@ sssp_status sssp_run_ex(sssp_handle* h, int32_t source, sssp_policy policy, uint
     if (!h) return set_error(SSSP_ERR_INVALID, "sssp_run: NULL handle");
     if (!d_dist_out) return set_error(SSSP_ERR_INVALID, "sssp_run: NULL d_dist_out");
     if (source < 0 || source >= h->n) return set_error(SSSP_ERR_RANGE, "sssp_run: source %d outside [0, %d)", source, h->n);
-    if (policy < SSSP_RHO || policy > SSSP_DIJKSTRA) return set_error(SSSP_ERR_INVALID, "sssp_run: unknown policy %d", (int)policy);
-    if ((policy == SSSP_RHO || policy == SSSP_DELTA) && param == 0)
+    if (policy < SSSP_RHO || policy > SSSP_DELTA_STEPPING) return set_error(SSSP_ERR_INVALID, "sssp_run: unknown policy %d", (int)policy);
+    if ((policy == SSSP_RHO || policy == SSSP_DELTA || policy == SSSP_DELTA_STEPPING) && param == 0)
         return set_error(SSSP_ERR_INVALID, "sssp_run: param (rho / Delta) must be >= 1");
     cudaError_t de = cudaSetDevice(h->device);
     if (de != cudaSuccess) return cuda_error(de, "cudaSetDevice");

@@ -14,9 +14,12 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 # (policy, param) per config: the bench defaults plus parameters that exercise other paths
 CASES = {
-    "grid256": [("rho", 1 << 12), ("rho", 1 << 21), ("delta", 1 << 13), ("bellman_ford", 0)],
-    "rmat20": [("rho", 1 << 15), ("rho", 1 << 18), ("delta", 1 << 13), ("bellman_ford", 0)],
-    "rgg4m": [("rho", 1 << 12), ("rho", 1 << 15), ("delta", 1 << 8), ("bellman_ford", 0)],
+    "grid256": [("rho", 1 << 12), ("rho", 1 << 21), ("delta", 1 << 13), ("bellman_ford", 0),
+                ("delta_stepping", 1 << 13)],
+    "rmat20": [("rho", 1 << 15), ("rho", 1 << 18), ("delta", 1 << 13), ("bellman_ford", 0),
+               ("delta_stepping", 1 << 13), ("dijkstra", 0)],
+    "rgg4m": [("rho", 1 << 12), ("rho", 1 << 15), ("delta", 1 << 8), ("bellman_ford", 0),
+              ("delta_stepping", 1 << 10)],
     "rmat24": [("rho", 1 << 15), ("rho", 1 << 18), ("rho", 1 << 21), ("delta", 1 << 15), ("bellman_ford", 0)],
     "grid4096": [("rho", 1 << 12), ("delta", 1 << 13), ("bellman_ford", 0)],
 }

@@ -37,7 +37,8 @@ def _assert_same(got, want, label):
 
 
 SMALL_POLICIES = [("rho", 1), ("rho", 3), ("rho", 64), ("rho", 1 << 21), ("delta", 1), ("delta", 77),
-                  ("delta", 4096), ("delta", 1 << 30), ("bellman_ford", 0), ("dijkstra", 0)]
+                  ("delta", 4096), ("delta", 1 << 30), ("bellman_ford", 0), ("dijkstra", 0),
+                  ("delta_stepping", 1), ("delta_stepping", 977), ("delta_stepping", 1 << 30)]
 
 
 def test_golden_examples(cuda_device):
@@ -168,6 +169,7 @@ def test_round_trace_parity(cuda_device, name):
     kn = int(hops.max())
     h = P.SSSP.from_graph(g)
     cases = [("bellman_ford", 0, {}), ("delta", 1000, {}), ("delta", 20000, {}), ("dijkstra", 0, {}),
+             ("delta_stepping", 1, {}), ("delta_stepping", 3000, {}),
              ("rho", 64, dict(exact=True, warmup=False)), ("rho", 2048, dict(exact=True, warmup=False)),
              ("rho", 512, dict(exact=True, warmup=True)), ("rho", 16, dict(exact=True, warmup=False)),
              ("rho", 64, dict(exact=True, warmup=False, nearfar=False))]
@@ -238,3 +240,24 @@ def test_determinism_and_run_host(cuda_device):
     d = h2.run(g.source, "delta", 1 << 14)
     s.synchronize()
     _assert_same(P.dist_to_u64(d), want, "side stream")
+
+
+def test_fusion_variants(cuda_device):
+    """Fusion (local relaxation within theta) on sparse graphs: any budget,
+    or none, gives the oracle's distances; the per-round |Q| identity still holds."""
+    P = _P()
+    for name in ("grid64", "rgg64k"):
+        g = gen.make(name)
+        want = oracle.dijkstra(g)
+        h = P.SSSP.from_graph(g)
+        for pol, par in (("rho", 64), ("rho", 4096), ("delta", 3000), ("delta_stepping", 3000), ("bellman_ford", 0)):
+            for kw in (dict(fuse=False), dict(fuse_budget=1), dict(fuse_budget=32), dict(fuse_budget=100000)):
+                d, st, tr, _ = h.run(g.source, pol, par, trace_cap=1 << 16, **kw)
+                _assert_same(P.dist_to_u64(d), want, f"{name}/{pol}/{par}/{kw}")
+                q = tr["qsize"]
+                assert (q[1:] == q[:-1] - tr["fsize"][:-1] + tr["inserts"][:-1]).all()
+        # fusion must cut the rounds of a high-diameter graph
+        h.run(g.source, "rho", 64, fuse=False)
+        r0 = h.last_stats["rounds"]
+        h.run(g.source, "rho", 64, fuse_budget=4096)
+        assert h.last_stats["rounds"] < r0
