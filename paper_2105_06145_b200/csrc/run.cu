@@ -81,6 +81,8 @@ constexpr int kQBuf = 256;                   // staged queue ids per warp (>= 32
 constexpr int kTBuf = 32 * kEnt + 32;        // staged extracted ids per warp
 constexpr int kFBuf = 32 * kArcs + 64;       // fused vertices waiting for their relax, per warp
 constexpr int kFuseBudget = SSSP_FUSE;       // fused vertices per warp per round (0 = off)
+constexpr int kFuseMaxDeg = 1024;            // a fused vertex of higher degree goes back to Q
+constexpr int kSparseDeg = 20;               // fusion in rounds whose frontier averages < 20 arcs
 constexpr int kShards = 32;                  // append-list segments (+1 spill)
 constexpr int kSeg = kShards + 1;
 constexpr int kCntStride = 256;              // int32 words between counters (1 KB: distinct L2 slices)
@@ -149,6 +151,7 @@ struct RunParams {
     int32_t* counters;  // [3 slots][2 lists: queue, chunks][kSeg] * kCntStride
     uint64_t* cta_min;  // [3 slots][kMaxCtas]: per-CTA min for Delta / Dijkstra
     int64_t* cta_delta; // [3 slots][kMaxCtas]: per-CTA change of |Q| (inserts - extractions)
+    int64_t* cta_front; // [3 slots][kMaxCtas]: per-CTA (arcs << 32 | vertices) extracted
     Desc* light;
     uint64_t* samples;
     Ctrl* ctrl;
@@ -289,6 +292,7 @@ struct Warp {  // per-warp working state (qn is warp-uniform)
     uint64_t fuse_theta;  // live rounds: theta (a vertex outside Q improved to <= theta is
                           // extracted on the spot, DESIGN.md §5 "fusion"); 0 = no fusion
     int64_t qdelta;       // this lane's inserts - extractions (|Q| bookkeeping)
+    uint64_t front;       // this lane's extractions: (arcs << 32) | vertices
     int shard;
     int32_t qn;
     int32_t fn;       // staged fused vertices (warp-uniform)
@@ -516,7 +520,21 @@ __device__ __forceinline__ void fuse_drain(const RunParams& p, Warp& W) {
         if (id >= 0) {
             beg = __ldg(p.off + id);
             deg = __ldg(p.off + id + 1) - beg;
+        }
+        // a fused hub goes back to Q instead (its arcs belong in chunks, not in one warp)
+        bool back = false;
+        const int32_t hub = id;
+        if (id >= 0 && deg > kFuseMaxDeg) {
+            const uint64_t old = atomicCAS((unsigned long long*)(p.dist + id), (unsigned long long)(d | kTop),
+                                           (unsigned long long)d);
+            back = old == (d | kTop) && admit<STATS>(old, d, W);  // else a later WriteMin re-inserted it
+            id = -1;
+            deg = 0;
+        }
+        wq_push1(W, back, hub);
+        if (id >= 0) {
             if (p.ext_count) atomicAdd(p.ext_count + id, 1);
+            W.front += 1 | ((uint64_t)deg << 32);
             if (STATS) {
                 W.acc.fused++;  // counted as inserted and extracted (the |Q| identity holds)
                 W.acc.inserts++;
@@ -583,8 +601,10 @@ __device__ __forceinline__ void take_batch(const RunParams& p, int32_t cnt, cons
     }
     if (id >= 0) {
         W.qdelta--;
+        W.front += 1;
         beg = __ldg(p.off + id);
         deg = __ldg(p.off + id + 1) - beg;
+        W.front += (uint64_t)deg << 32;
         if (p.ext_count) atomicAdd(p.ext_count + id, 1);
     }
     if (STATS && id >= 0) {
@@ -718,6 +738,10 @@ __device__ __forceinline__ void flush_acc(const RunParams& p, int64_t r, Warp& W
     if (lane_id() == 0 && dq) atomicAdd((unsigned long long*)(p.cta_delta + (r % 3) * kMaxCtas + blockIdx.x),
                                         (unsigned long long)dq);
     W.qdelta = 0;
+    const uint64_t fr = warp_sum(W.front);
+    if (lane_id() == 0 && fr) atomicAdd((unsigned long long*)(p.cta_front + (r % 3) * kMaxCtas + blockIdx.x),
+                                        (unsigned long long)fr);
+    W.front = 0;
     if (STATS) {
         const uint32_t s = warp_sum(W.acc.succ), ins = warp_sum(W.acc.inserts), fu = warp_sum(W.acc.fused);
         const uint64_t fe = warp_sum(W.acc.fused_edges);
@@ -847,6 +871,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     __shared__ int64_t cpref[kSeg + 1];  // segment prefix of the round's chunk list
     __shared__ uint64_t bc_u[3];         // min_Q (Delta / Dijkstra), CTA-0 theta, CTA-0 split
     __shared__ int64_t bc_dq;
+    __shared__ uint64_t bc_front;
     __shared__ int32_t bc_nl, bc_cnt;
     __shared__ uint64_t red[kWarps];
     Ctrl* ctrl = p.ctrl;
@@ -857,6 +882,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     W.qn = 0;
     W.fn = 0;
     W.qdelta = 0;
+    W.front = 0;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
 
@@ -868,6 +894,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     for (int64_t i = gtid; i < 3 * kMaxCtas; i += gsize) {
         p.cta_min[i] = kInf;
         p.cta_delta[i] = 0;
+        p.cta_front[i] = 0;
     }
     if (gtid == 0) {
         p.qbuf[1][0] = p.source;  // Q_1 lives in qbuf[1], shard 0
@@ -897,6 +924,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         const Sharded<int32_t> QC = queue_of(p, r);
         const Sharded<Desc> CL = chunks_of(p, r);
         // |Q_r| = |Q_{r-1}| + sum over CTAs of (inserts - extractions) in round r-1
+        if ((threadIdx.x >> 5) == 2 && r > 1) {  // warp 2: the previous round's frontier size and arcs
+            const int lane = lane_id();
+            const int64_t* cf = p.cta_front + ((r + 2) % 3) * kMaxCtas;
+            uint64_t sf = 0;
+            for (int i = lane; i < (int)gridDim.x; i += 32) sf += __ldcg((const unsigned long long*)(cf + i));
+            sf = warp_sum(sf);
+            if (lane == 0) bc_front = sf;
+        }
         if ((threadIdx.x >> 5) == 1 && r > 1) {  // warp 1, in parallel with warp 0's load_prefix
             const int lane = lane_id();
             const int64_t* cd = p.cta_delta + ((r + 2) % 3) * kMaxCtas;
@@ -920,7 +955,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         if (gtid < 2 * kSeg) {  // counters of slot (r+1)%3: written in round r+1, read in r+1 / r+2
             p.counters[((int64_t)(((r + 1) % 3) * 2) * kSeg + gtid) * kCntStride] = 0;
         }
-        if (threadIdx.x == 0) p.cta_delta[((r + 1) % 3) * kMaxCtas + blockIdx.x] = 0;
+        if (threadIdx.x == 0) {
+            p.cta_delta[((r + 1) % 3) * kMaxCtas + blockIdx.x] = 0;
+            p.cta_front[((r + 1) % 3) * kMaxCtas + blockIdx.x] = 0;
+        }
         W.qnext = queue_of(p, r + 1);
         W.C = C;
 
@@ -1050,7 +1088,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             }
         }
         W.split = split;
-        W.fuse_theta = snap ? 0 : theta;  // fusion only in live rounds
+        // fusion in live rounds that are sparse: a sparse graph, or a previous frontier that
+        // averaged fewer than 20 arcs per vertex (the paper's rule)
+        const uint64_t fv = r > 1 ? (bc_front & 0xFFFFFFFFull) : 1, fe = r > 1 ? (bc_front >> 32) : 0;
+        const bool sparse = p.m < (int64_t)kSparseDeg * p.n || fe < (uint64_t)kSparseDeg * fv;
+        W.fuse_theta = (snap || !sparse) ? 0 : theta;
         W.fbudget = p.fuse_budget;
         if (STATS && gtid == 0) t1 = globaltimer();
 
@@ -1168,6 +1210,7 @@ struct Layout {
     int32_t* counters;
     uint64_t* cta_min;
     int64_t* cta_delta;
+    int64_t* cta_front;
     Desc* light;
     uint64_t* samples;
     Ctrl* ctrl;
@@ -1190,6 +1233,7 @@ Layout carve(void* base, int32_t n, int64_t m) {
     L.counters = c.take<int32_t>((size_t)3 * 2 * kSeg * kCntStride);
     L.cta_min = c.take<uint64_t>((size_t)3 * kMaxCtas);
     L.cta_delta = c.take<int64_t>((size_t)3 * kMaxCtas);
+    L.cta_front = c.take<int64_t>((size_t)3 * kMaxCtas);
     L.dist = c.take<uint64_t>(n);
     L.q0 = c.take<int32_t>(qlen);
     L.q1 = c.take<int32_t>(qlen);
@@ -1282,6 +1326,7 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
     b.counters = L.counters;
     b.cta_min = L.cta_min;
     b.cta_delta = L.cta_delta;
+    b.cta_front = L.cta_front;
     b.light = L.light;
     b.samples = L.samples;
     b.ctrl = L.ctrl;
@@ -1350,8 +1395,10 @@ sssp_status sssp_run_ex(sssp_handle* h, int32_t source, sssp_policy policy, uint
     const bool st = (o.flags & SSSP_RUN_STATS) != 0;
     // fusion ("local relaxation within theta") in live rounds of sparse graphs:
     // the paper applies it when the average degree is below 20
+    // (measured: fusing the low-degree late rounds of R-MAT re-relaxes 17% more arcs and
+    // costs 50% time, so dense graphs do not fuse at all; see DESIGN.md fusion)
     const bool fu = !(o.flags & (SSSP_RUN_SNAPSHOT | SSSP_RUN_NO_FUSE)) && policy != SSSP_DIJKSTRA &&
-                    h->m < 20 * (int64_t)h->n;
+                    h->m < (int64_t)kSparseDeg * h->n;
     RunParams p = h->base;
     p.dist = d_dist_out;
     p.source = source;
