@@ -129,6 +129,8 @@ typedef struct {
     int64_t t_relax_ns;   /* device time of the remaining relax phase                 */
     int64_t qnear;        /* ids listed in the queue array (near part of Q) and scanned  */
     int64_t dense;        /* vertices read by near/far dense passes this round           */
+    int64_t busy_a_ns;    /* sum over warps of time spent in phase A before its barrier  */
+    int64_t busy_b_ns;    /* sum over warps of time spent in phase B before its barrier  */
 } sssp_round;
 
 typedef struct {

@@ -82,6 +82,10 @@ constexpr int kTBuf = 32 * kEnt + 32;        // staged extracted ids per warp
 constexpr int kFBuf = 32 * kArcs + 64;       // fused vertices waiting for their relax, per warp
 constexpr int kFuseBudget = SSSP_FUSE;       // fused vertices per warp per round (0 = off)
 constexpr int kFuseMaxDeg = 1024;            // a fused vertex of higher degree goes back to Q
+#ifndef SSSP_CONTIG
+#define SSSP_CONTIG 16
+#endif
+constexpr int kContigTiles = SSSP_CONTIG;    // queue < kContigTiles*32 ids per warp: contiguous shares
 constexpr int kSparseDeg = 20;               // fusion in rounds whose frontier averages < 20 arcs
 constexpr int kShards = 32;                  // append-list segments (+1 spill)
 constexpr int kSeg = kShards + 1;
@@ -110,7 +114,9 @@ struct __align__(128) RoundCnt {
     unsigned long long succ;     // STATS: successful WriteMins
     unsigned long long inserts;  // STATS: ids inserted into Q by relax
     unsigned long long split;    // CTA-0 broadcast of a new near/far split
-    unsigned long long pad[9];
+    unsigned long long busy_a;   // STATS: sum over warps of phase-A busy time (ns)
+    unsigned long long busy_b;   // STATS: same for phase B
+    unsigned long long pad[7];
 };
 
 struct __align__(128) Ctrl {
@@ -185,6 +191,8 @@ __device__ __forceinline__ void reset_cnt(RoundCnt* c) {
     c->succ = 0;
     c->inserts = 0;
     c->split = 0;
+    c->busy_a = 0;
+    c->busy_b = 0;
 }
 
 __device__ __forceinline__ Desc ld_desc(const Desc* p) {
@@ -634,7 +642,15 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
     // kEnt entries per lane only when every warp gets at least two such steps; small
     // queues are spread one entry per lane so that more warps share the round
     const int ent = q >= nwarps * (32 * kEnt) ? kEnt : 1;
-    for (int64_t base = gw * (32 * ent); base < q; base += nwarps * (32 * ent)) {
+    // Small queues: an equal contiguous share per warp (+-1 entry).  A round lasts as long
+    // as its slowest warp; strided tiles left some warps with 3 tiles and others with 1,
+    // and contiguous ids (appended together) keep a warp's fusion local.  Large queues:
+    // strided tiles, since ids appended together carry correlated work (R-MAT hubs).
+    const bool contig = q < (int64_t)kContigTiles * 32 * nwarps;
+    const int64_t lo = contig ? gw * q / nwarps : gw * (32 * ent);
+    const int64_t hi = contig ? (gw + 1) * q / nwarps : q;
+    const int64_t stride = contig ? 32 * ent : nwarps * (32 * ent);
+    for (int64_t base = lo; base < hi; base += stride) {
         int32_t id[kEnt];
         uint64_t val[kEnt];
         const int sg = seg_of(qpref, base);  // warp-uniform
@@ -642,7 +658,7 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
         for (int e = 0; e < kEnt; e++) {
             const int64_t i = base + e * 32 + lane;
             id[e] = -1;
-            if (e < ent && i < q) {
+            if (e < ent && i < hi) {
                 int s = sg;
                 while (qpref[s + 1] <= i) s++;
                 id[e] = ld_cg_i32(QC.seg(s) + (i - qpref[s]));
@@ -1098,7 +1114,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
 
         // ---- phase A: Extract(theta) (+ light relax in live mode)
         uint64_t minrem = kInf;
+        const uint64_t ta = STATS ? globaltimer() : 0;
         phase_a<POL, STATS, FUSE>(p, QC, qpref, CL, theta, snap, minrem, W);
+        if (STATS && lane_id() == 0) atomicAdd(&C->busy_a, (unsigned long long)(globaltimer() - ta));
         flush_acc<POL, STATS, FUSE>(p, r, W);
         grid_sync(nullptr);
         if (STATS && gtid == 0) t2 = globaltimer();
@@ -1108,7 +1126,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         __syncthreads();
         const int32_t nl = bc_nl;
         const bool phase_b_work = cpref[kSeg] + nl > 0;
-        if (phase_b_work) phase_b<POL, STATS, FUSE>(p, CL, cpref, nl, W);
+        if (phase_b_work) {
+            const uint64_t tb = STATS ? globaltimer() : 0;
+            phase_b<POL, STATS, FUSE>(p, CL, cpref, nl, W);
+            if (STATS && lane_id() == 0) atomicAdd(&C->busy_b, (unsigned long long)(globaltimer() - tb));
+        }
         if (uses_min(POL)) {  // this CTA's min over kept ids and successful WriteMins
             uint64_t mn = warp_min_u64(minrem < W.acc.minsucc ? minrem : W.acc.minsucc);
             if (lane_id() == 0) red[threadIdx.x >> 5] = mn;
@@ -1143,6 +1165,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                 t->t_relax_ns = (int64_t)(t3 - t2);
                 t->qnear = qn;
                 t->dense = dense;
+                t->busy_a_ns = (int64_t)C->busy_a;
+                t->busy_b_ns = (int64_t)C->busy_b;
             }
             ctrl->tot_extracted += f;
             ctrl->tot_edges += (int64_t)C->edges;
