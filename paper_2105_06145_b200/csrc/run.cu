@@ -71,7 +71,7 @@ constexpr int kWarps = kBlock / 32;
 #define SSSP_L1DIST 1
 #endif
 #ifndef SSSP_FUSE
-#define SSSP_FUSE 256
+#define SSSP_FUSE 64
 #endif
 #ifndef SSSP_ENT
 #define SSSP_ENT 2
