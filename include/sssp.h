@@ -50,7 +50,8 @@ typedef enum {
     SSSP_ERR_CAPACITY = -4,      /* output buffer too small; the queue is left unchanged             */
     SSSP_ERR_CUDA = -5,          /* a CUDA runtime call or kernel failed                              */
     SSSP_ERR_ROUNDS = -6,        /* max_rounds exceeded (distances are then NOT final)                */
-    SSSP_ERR_DEVICE = -7         /* no usable sm_100 device / cooperative launch unsupported          */
+    SSSP_ERR_DEVICE = -7,        /* no usable sm_100 device / cooperative launch unsupported          */
+    SSSP_ERR_INTERNAL = -8       /* a device-side capacity guard fired (a bug; distances not final)   */
 } sssp_status;
 
 /* ExtDist rules of Table tab:framework.  FinishCheck is empty for all. */

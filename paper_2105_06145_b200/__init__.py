@@ -26,7 +26,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 INF = 0xFFFFFFFFFFFFFFFF
 SSSP_OK, SSSP_ERR_INVALID, SSSP_ERR_INVALID_GRAPH, SSSP_ERR_RANGE = 0, -1, -2, -3
-SSSP_ERR_CAPACITY, SSSP_ERR_CUDA, SSSP_ERR_ROUNDS, SSSP_ERR_DEVICE = -4, -5, -6, -7
+SSSP_ERR_CAPACITY, SSSP_ERR_CUDA, SSSP_ERR_ROUNDS, SSSP_ERR_DEVICE, SSSP_ERR_INTERNAL = -4, -5, -6, -7, -8
 SSSP_RHO, SSSP_DELTA, SSSP_BELLMAN_FORD, SSSP_DIJKSTRA, SSSP_DELTA_STEPPING = 0, 1, 2, 3, 4
 POLICIES = {"rho": SSSP_RHO, "delta": SSSP_DELTA, "bellman_ford": SSSP_BELLMAN_FORD, "bf": SSSP_BELLMAN_FORD,
             "dijkstra": SSSP_DIJKSTRA, "delta_stepping": SSSP_DELTA_STEPPING}

@@ -34,6 +34,7 @@ const char* sssp_status_string(sssp_status s) {
         case SSSP_ERR_CUDA: return "SSSP_ERR_CUDA";
         case SSSP_ERR_ROUNDS: return "SSSP_ERR_ROUNDS";
         case SSSP_ERR_DEVICE: return "SSSP_ERR_DEVICE";
+        case SSSP_ERR_INTERNAL: return "SSSP_ERR_INTERNAL";
     }
     return "SSSP_ERR_UNKNOWN";
 }

@@ -133,8 +133,10 @@ struct __align__(128) Ctrl {
 template <typename T>
 struct Sharded {
     T* base;
-    int32_t* cnt;  // cnt[s * kCntStride]
-    int64_t cap;   // per-shard capacity
+    int32_t* cnt;       // cnt[s * kCntStride]
+    int64_t cap;        // per-shard capacity
+    int64_t spill_cap;  // capacity of the spill segment
+    int32_t* err;       // set to SSSP_ERR_INTERNAL if a reservation ever exceeded the spill
     __device__ __forceinline__ T* seg(int s) const { return base + (int64_t)s * cap; }
     __device__ __forceinline__ int64_t seg_count(int s) const {
         const int64_t c = __ldcg(cnt + s * kCntStride);
@@ -154,6 +156,7 @@ struct RunParams {
     int64_t qcap;       // per-shard queue capacity
     Desc* chunks;       // chunk descriptor storage
     int64_t ccap;       // per-shard chunk capacity
+    int64_t cspill;     // chunk spill capacity
     int32_t* counters;  // [3 slots][2 lists: queue, chunks][kSeg] * kCntStride
     uint64_t* cta_min;  // [3 slots][kMaxCtas]: per-CTA min for Delta / Dijkstra
     int64_t* cta_delta; // [3 slots][kMaxCtas]: per-CTA change of |Q| (inserts - extractions)
@@ -176,10 +179,11 @@ __device__ __forceinline__ int32_t* counters_of(const RunParams& p, int slot, in
 }
 __device__ __forceinline__ Sharded<int32_t> queue_of(const RunParams& p, int64_t round_of_queue) {
     // Q_r lives in qbuf[r & 1]; its counts are in slot (r + 2) % 3
-    return Sharded<int32_t>{p.qbuf[round_of_queue & 1], counters_of(p, (int)((round_of_queue + 2) % 3), 0), p.qcap};
+    return Sharded<int32_t>{p.qbuf[round_of_queue & 1], counters_of(p, (int)((round_of_queue + 2) % 3), 0), p.qcap,
+                            (int64_t)p.n, &p.ctrl->status};
 }
 __device__ __forceinline__ Sharded<Desc> chunks_of(const RunParams& p, int64_t r) {
-    return Sharded<Desc>{p.chunks, counters_of(p, (int)(r % 3), 1), p.ccap};
+    return Sharded<Desc>{p.chunks, counters_of(p, (int)(r % 3), 1), p.ccap, p.cspill, &p.ctrl->status};
 }
 
 __device__ __forceinline__ void reset_cnt(RoundCnt* c) {
@@ -323,8 +327,12 @@ __device__ __forceinline__ bool admit(uint64_t w_old, uint64_t c, Warp& W) {
 
 // Reserve `tot` slots of a sharded list for this warp (lane 0 does the atomics).
 // Element i < tot goes to p0 + i if i < fit, else to p1 + (i - fit) (spill segment).
+// The capacities make overflow impossible (a list never holds more than its bound), but a
+// reservation past the spill segment is still refused: `lim` < tot elements are writable
+// and the run fails with SSSP_ERR_INTERNAL instead of corrupting memory.
 template <typename T>
-__device__ __forceinline__ void reserve(const Sharded<T>& L, int shard, int32_t tot, T*& p0, int32_t& fit, T*& p1) {
+__device__ __forceinline__ void reserve(const Sharded<T>& L, int shard, int32_t tot, T*& p0, int32_t& fit, T*& p1,
+                                        int32_t& lim) {
     int64_t pos = 0, spos = 0;
     if (lane_id() == 0) {
         pos = atomicAdd(L.cnt + shard * kCntStride, tot);
@@ -334,6 +342,9 @@ __device__ __forceinline__ void reserve(const Sharded<T>& L, int shard, int32_t 
     pos = __shfl_sync(kFull, pos, 0);
     spos = __shfl_sync(kFull, spos, 0);
     fit = pos >= L.cap ? 0 : (int32_t)(L.cap - pos < tot ? L.cap - pos : tot);
+    const int64_t room = L.spill_cap - spos;
+    lim = fit + (int32_t)(room <= 0 ? 0 : (room < tot - fit ? room : tot - fit));
+    if (lim < tot && lane_id() == 0) atomicExch(L.err, (int32_t)SSSP_ERR_INTERNAL);
     p0 = L.seg(shard) + pos;
     p1 = L.seg(kShards) + spos;
 }
@@ -342,9 +353,9 @@ __device__ __forceinline__ void wq_flush(Warp& W) {
     if (W.qn == 0) return;
     __syncwarp();
     int32_t *p0, *p1;
-    int32_t fit;
-    reserve(W.qnext, W.shard, W.qn, p0, fit, p1);
-    for (int32_t i = lane_id(); i < W.qn; i += 32) {
+    int32_t fit, lim;
+    reserve(W.qnext, W.shard, W.qn, p0, fit, p1, lim);
+    for (int32_t i = lane_id(); i < lim; i += 32) {
         const int32_t v = W.st->q[i];
         if (i < fit)
             p0[i] = v;
@@ -565,8 +576,8 @@ __device__ __forceinline__ void emit_chunks(const Sharded<Desc>& CL, int shard, 
     const int32_t excl = incl - nch;
     if (stats && lane == 0) atomicAdd(&C->nheavy, __popc(hm));
     Desc *p0, *p1;
-    int32_t fit;
-    reserve(CL, shard, tot, p0, fit, p1);
+    int32_t fit, lim;
+    reserve(CL, shard, tot, p0, fit, p1, lim);
     for (int32_t j0 = 0; j0 < tot; j0 += 32) {
         const int32_t j = j0 + lane;
         int32_t o = 0;
@@ -579,7 +590,7 @@ __device__ __forceinline__ void emit_chunks(const Sharded<Desc>& CL, int shard, 
         const int32_t oe = __shfl_sync(kFull, excl, o);
         const int32_t od = __shfl_sync(kFull, deg, o);
         const uint64_t odd = __shfl_sync(kFull, d, o);
-        if (j < tot) {
+        if (j < lim) {
             const int32_t k = (j - oe) * kChunk;
             st_desc(j < fit ? p0 + j : p1 + (j - fit), odd, ob + k, min(kChunk, od - k));
         }
@@ -1231,6 +1242,7 @@ struct Layout {
     int64_t qcap;
     Desc* chunks;
     int64_t ccap;
+    int64_t cspill;
     int32_t* counters;
     uint64_t* cta_min;
     int64_t* cta_delta;
@@ -1251,6 +1263,7 @@ Layout carve(void* base, int32_t n, int64_t m) {
     // chunks per round <= sum over heavy extracted vertices of ceil(deg/kChunk)
     const int64_t ctot = m / kChunk + std::min<int64_t>(n, m / (kLight + 1)) + 1;
     L.ccap = 2 * ((ctot + kShards - 1) / kShards) + 256;
+    L.cspill = ctot;
     const int64_t clen = kShards * L.ccap + ctot;
     L.ctrl = c.take<Ctrl>(1);
     L.err = c.take<int32_t>(32);
@@ -1347,6 +1360,7 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
     b.qcap = L.qcap;
     b.chunks = L.chunks;
     b.ccap = L.ccap;
+    b.cspill = L.cspill;
     b.counters = L.counters;
     b.cta_min = L.cta_min;
     b.cta_delta = L.cta_delta;
@@ -1465,6 +1479,8 @@ sssp_status sssp_run_ex(sssp_handle* h, int32_t source, sssp_policy policy, uint
     }
     if (c->status == SSSP_ERR_ROUNDS)
         return set_error(SSSP_ERR_ROUNDS, "sssp_run: exceeded max_rounds=%lld", (long long)p.max_rounds);
+    if (c->status == SSSP_ERR_INTERNAL)
+        return set_error(SSSP_ERR_INTERNAL, "sssp_run: an append list overflowed its spill segment (bug)");
     return SSSP_OK;
 }
 

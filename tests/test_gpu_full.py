@@ -47,3 +47,26 @@ def test_full_config(cuda_device, name):
         assert h.last_stats["rounds"] >= kn + 1
         if pol == "bellman_ford":
             assert h.last_stats["rounds"] == kn + 1
+
+
+def test_large_id_space(cuda_device):
+    """n = 2^27 with the reachable part spread over the whole id range: 64-bit index math
+    in the queue, chunk and output paths (ids above 2^26 and near n-1)."""
+    import paper_2105_06145_b200 as P
+
+    n = 1 << 27
+    rs = np.random.default_rng(27)
+    k = 3000
+    ids = np.sort(rs.choice(n, size=k, replace=False)).astype(np.int64)
+    ids[-1] = n - 1
+    src = np.concatenate([ids[:-1], ids[rs.integers(0, k, 4 * k)]])
+    dst = np.concatenate([ids[1:], ids[rs.integers(0, k, 4 * k)]])
+    w = rs.integers(1, 1 << 20, len(src)).astype(np.uint32)
+    keep = src != dst
+    g = gen.from_arcs(n, src[keep], dst[keep], w[keep], symmetrise=True, source=int(ids[0]))
+    want = oracle.dijkstra(g)
+    h = P.SSSP.from_graph(g)
+    for pol, par in (("rho", 64), ("delta", 1 << 18), ("bellman_ford", 0), ("delta_stepping", 1 << 18)):
+        got = P.dist_to_u64(h.run(g.source, pol, par))
+        assert np.array_equal(got, want), pol
+    h.close()
