@@ -103,6 +103,10 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t *d_offsets, const in
                                  fewer barriers; distances are identical, round counts may differ.     */
 #define SSSP_RUN_NO_FUSE 32u    /* live rounds on sparse graphs (m < 20 n): do not extract a vertex
                                    improved to <= theta on the spot (DESIGN.md fusion) */
+#define SSSP_RUN_BIDIR 64u      /* UNDIRECTED graphs only (the caller guarantees every arc (u,v,w) has
+                                   its reverse (v,u,w)): a light vertex first pulls
+                                   delta[u] <- min_v delta[v] + w(v,u) over its arcs, then pushes
+                                   (DESIGN.md bidirectional)                          */
 #define SSSP_RUN_NO_NEARFAR 16u /* rho: list all of Q in the queue array every round instead of only
                                    its near part (keys <= split; DESIGN.md §5 near/far)              */
 

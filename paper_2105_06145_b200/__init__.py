@@ -32,7 +32,7 @@ POLICIES = {"rho": SSSP_RHO, "delta": SSSP_DELTA, "bellman_ford": SSSP_BELLMAN_F
             "dijkstra": SSSP_DIJKSTRA, "delta_stepping": SSSP_DELTA_STEPPING}
 SSSP_VALIDATE = 1
 SSSP_RUN_RHO_EXACT, SSSP_RUN_NO_WARMUP, SSSP_RUN_STATS, SSSP_RUN_SNAPSHOT, SSSP_RUN_NO_NEARFAR = 1, 2, 4, 8, 16
-SSSP_RUN_NO_FUSE = 32
+SSSP_RUN_NO_FUSE, SSSP_RUN_BIDIR = 32, 64
 SSSP_SELECT_SAMPLED, SSSP_SELECT_EXACT = 0, 1
 
 
@@ -157,7 +157,7 @@ class SSSP:
 
     def run(self, source, policy="rho", param=0, out=None, stats=False, trace_cap=0, ext_counts=False,
             exact=False, warmup=True, seed=0, max_rounds=0, snapshot=False, nearfar=True, fuse=True,
-            fuse_budget=0):
+            fuse_budget=0, bidir=False):
         """Alg. 1 from `source`; returns a uint64-valued int64 tensor of distances (INF = -1 as int64).
 
         With stats=True returns (dist, stats_dict, trace ndarray | None, ext_count tensor | None)."""
@@ -168,7 +168,8 @@ class SSSP:
         o = sssp_run_opts()
         o.flags = (SSSP_RUN_RHO_EXACT if exact else 0) | (0 if warmup else SSSP_RUN_NO_WARMUP) | \
                   (SSSP_RUN_STATS if (stats or trace_cap) else 0) | (SSSP_RUN_SNAPSHOT if snapshot else 0) | \
-                  (0 if nearfar else SSSP_RUN_NO_NEARFAR) | (0 if fuse else SSSP_RUN_NO_FUSE)
+                  (0 if nearfar else SSSP_RUN_NO_NEARFAR) | (0 if fuse else SSSP_RUN_NO_FUSE) | \
+            (SSSP_RUN_BIDIR if bidir else 0)
         o.fuse_budget = fuse_budget
         o.seed = seed
         o.max_rounds = max_rounds

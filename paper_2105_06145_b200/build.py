@@ -1,50 +1,86 @@
-"""Build libsssp.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+"""Build libsssp.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+The round-loop kernel template (csrc/loop.cuh) is instantiated per (policy, bidirectional)
+pair: csrc/inst.cu is compiled once per pair with -DINST_POL/-DINST_BIDIR, in parallel with
+the other translation units, and everything is linked into one shared library.
+"""
 from __future__ import annotations
 
 import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsssp.so")
 
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+POLICIES = 5  # SSSP_RHO .. SSSP_DELTA_STEPPING (include/sssp.h)
 
 
-def sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+def units():
+    """(name, source, extra defines) for every object file of the library."""
+    out = [(os.path.splitext(os.path.basename(s))[0], s, []) for s in sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+           if os.path.basename(s) != "inst.cu"]
+    inst = os.path.join(CSRC, "inst.cu")
+    for pol in range(POLICIES):
+        for bidir in (0, 1):
+            out.append((f"inst_{pol}_{bidir}", inst, [f"-DINST_POL={pol}", f"-DINST_BIDIR={bidir}"]))
+    return out
 
 
 def deps():
-    return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))) + [
-        os.path.join(HERE, "..", "include", "sssp.h")]
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+                  glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(HERE, "..", "include", "sssp.h")]
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(OUT):
+def up_to_date(out: str = OUT) -> bool:
+    if not os.path.exists(out):
         return False
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
 def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=()) -> str:
-    """Compile every csrc/*.cu into one shared library (defines: tuning variants, e.g. SSSP_ARCS=4)."""
+    """Compile every translation unit (in parallel) and link the shared library.
+    defines: tuning variants, e.g. SSSP_ARCS=4 (written to a separate `out`)."""
     if not force and out == OUT and not defines and up_to_date():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", out, *sources()]
+    tag = os.path.splitext(os.path.basename(out))[0]
+    objdir = os.path.join(HERE, "build", tag)
+    os.makedirs(objdir, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
+
+    def compile_one(u):
+        name, src, extra = u
+        obj = os.path.join(objdir, name + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *dflags, *extra, "-c", "-o", obj, src]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        return name, obj, cmd, res
+
+    jobs = int(os.environ.get("SSSP_BUILD_JOBS", str(os.cpu_count() or 4)))
+    with ThreadPoolExecutor(max_workers=max(1, jobs)) as ex:
+        results = list(ex.map(compile_one, units()))
+    log_path = os.path.join(HERE, "build.log" if out == OUT else os.path.basename(out) + ".log")
+    with open(log_path, "w") as log:
+        for name, obj, cmd, res in results:
+            log.write(f"### {name}: {' '.join(cmd)}\n{res.stdout}{res.stderr}\n")
+    failed = [(n, r) for n, _, _, r in results if r.returncode != 0]
+    if failed:
+        for n, r in failed:
+            sys.stderr.write(f"--- {n}\n{r.stdout}{r.stderr}")
+        raise RuntimeError(f"nvcc failed for {[n for n, _ in failed]}; see {log_path}")
+    link = [nvcc, *ARCH, "-shared", "-o", out, *[obj for _, obj, _, _ in results]]
     if verbose:
-        print(" ".join(cmd), flush=True)
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(HERE, "build.log" if out == OUT else os.path.basename(out) + ".log")
-    with open(log, "w") as f:
-        f.write(res.stdout + res.stderr)
+        print(" ".join(link), flush=True)
+    res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
+        raise RuntimeError(f"link failed ({res.returncode})")
     return out
 
 

@@ -1,0 +1,1273 @@
+// loop.cuh — the stepping-algorithm round loop (Alg. 1) as ONE persistent
+// cooperative kernel template.  Included by inst.cu (compiled once per policy and
+// bidirectional flag, in parallel) and by run.cu (host API: layout and launch only).
+//
+// LaB-PQ of the round loop: the membership flag of a vertex lives in
+// the top bit of its delta word (bit 63 set = NOT in Q), the value in the low 63
+// bits; the queue is a compacted id array (ping-pong per round).
+//   Update(v)   = the WriteMin CAS that lowers the value also clears bit 63; the
+//                 thread whose CAS saw bit 63 set appends v (exactly one append per
+//                 insertion, no duplicates).
+//   Extract(u)  = atomicOr(bit 63): deletes u from Q and returns, atomically, the
+//                 value it is relaxed with (its snapshot key).
+// Because flag and key share one word, a concurrent WriteMin and Extract can never
+// lose an update, so Extract and relax may overlap ("live" rounds, the default).
+//
+// Append lists (next queue, heavy-chunk descriptors) are SHARDED: kShards segments,
+// each with its own counter on its own L2 slice, plus a spill segment.  Same-address
+// atomics serialise in the L2 (~7 ns each), so one shared tail counter capped the
+// queue scan at ~0.5 TB/s; warps stage appends in shared memory and reserve space in
+// their shard once per <= 256 ids.  Readers see a list as the concatenation of its
+// segments (prefix of the segment counts, computed per CTA in shared memory).
+//
+// Per round r:
+//   ExtDist  theta_r per policy (Table tab:framework).  rho: every CTA
+//            draws the same counter-based samples into shared memory and selects
+//            the same theta (readings R5/R6) -> no barrier.
+//   Phase A  one pass over the queue (array LaB-PQ P:1011-1012): ids with
+//            key <= theta are extracted; vertices of degree <= kLight are relaxed by
+//            the extracting warp (live) or listed (snapshot mode); heavier ones are
+//            cut into kChunk-arc descriptors; the rest of Q is compacted into the
+//            next queue.                                              grid barrier
+//   Phase B  warps stride over the chunk descriptors (and, in snapshot mode, the
+//            light list): per arc c = d_u + w, plain L2 load filter, WriteMin by CAS
+//            (P:697), append on insertion.          grid barrier (only if non-empty)
+//   loop while |Q| > 0.
+#pragma once
+#include <stdio.h>
+
+#include <algorithm>
+#include <string.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace sssp {
+
+#ifndef SSSP_MIN_BLOCKS
+#define SSSP_MIN_BLOCKS 1
+#endif
+#ifndef SSSP_BLOCK
+#define SSSP_BLOCK 1024
+#endif
+#ifndef SSSP_ARCS
+#define SSSP_ARCS 4
+#endif
+#ifndef SSSP_LIGHT
+#define SSSP_LIGHT 128
+#endif
+constexpr uint64_t kTop = 1ull << 63;        // flag bit: set = not in Q
+constexpr uint64_t kVal = kTop - 1;          // value bits of a delta word
+constexpr int kBlock = SSSP_BLOCK;           // threads per CTA of the round loop
+constexpr int kMinBlocks = SSSP_MIN_BLOCKS;  // CTAs per SM the register budget targets
+constexpr int kArcs = SSSP_ARCS;             // arcs per lane in flight
+constexpr int kChunk = 32 * kArcs;           // arcs per heavy-chunk descriptor
+constexpr int kLight = SSSP_LIGHT;           // out-degree <= kLight: relaxed by the extracting warp
+constexpr int kSmemSamples = 2048;           // theta samples held in shared memory (else CTA-0 fallback)
+constexpr int kRankSelect = 256;             // s <= this: select by rank counting
+constexpr int kWarps = kBlock / 32;
+#ifndef SSSP_NEAR_K
+#define SSSP_NEAR_K 4
+#endif
+#ifndef SSSP_L1DIST
+#define SSSP_L1DIST 1
+#endif
+#ifndef SSSP_FUSE
+#define SSSP_FUSE 64
+#endif
+#ifndef SSSP_ENT
+#define SSSP_ENT 2
+#endif
+constexpr int kEnt = SSSP_ENT;               // queue entries per lane per Extract step (large queues)
+constexpr int kQBuf = 256;                   // staged queue ids per warp (>= 32 * kArcs)
+constexpr int kTBuf = 32 * kEnt + 32;        // staged extracted ids per warp
+constexpr int kFBuf = 32 * kArcs + 64;       // fused vertices waiting for their relax, per warp
+constexpr int kFuseBudget = SSSP_FUSE;       // fused vertices per warp per round (0 = off)
+constexpr int kFuseMaxDeg = 1024;            // a fused vertex of higher degree goes back to Q
+#ifndef SSSP_CONTIG
+#define SSSP_CONTIG 16
+#endif
+constexpr int kContigTiles = SSSP_CONTIG;    // queue < kContigTiles*32 ids per warp: contiguous shares
+constexpr int kSparseDeg = 20;               // fusion in rounds whose frontier averages < 20 arcs
+constexpr int kShards = 32;                  // append-list segments (+1 spill)
+constexpr int kSeg = kShards + 1;
+constexpr int kCntStride = 256;              // int32 words between counters (1 KB: distinct L2 slices)
+constexpr int kMaxCtas = 4096;
+constexpr int kPolicies = 5;
+constexpr int kNearK = SSSP_NEAR_K;          // near queue target: ~kNearK rounds of extraction
+constexpr int kFarSamples = 1024;            // vertices probed to place a new near/far split
+static_assert(32 * kArcs <= kQBuf, "one relax step must fit the stage");
+static_assert(kBlock % 32 == 0 && kBlock <= 1024, "block size");
+
+// A vertex (or a piece of one) to relax: snapshot key and a CSR arc range.
+struct __align__(16) Desc {
+    uint64_t d;
+    int32_t beg;
+    int32_t len;
+};
+
+// Per-round control (triple-buffered by round slot).
+struct __align__(128) RoundCnt {
+    int32_t nlight;              // snapshot mode: light frontier entries
+    int32_t nheavy;              // STATS: heavy vertices
+    unsigned long long theta;    // CTA-0 fallback theta
+    unsigned long long fsize;    // STATS: extracted
+    unsigned long long edges;    // STATS: arcs of extracted vertices
+    unsigned long long succ;     // STATS: successful WriteMins
+    unsigned long long inserts;  // STATS: ids inserted into Q by relax
+    unsigned long long split;    // CTA-0 broadcast of a new near/far split
+    unsigned long long busy_a;   // STATS: sum over warps of phase-A busy time (ns)
+    unsigned long long busy_b;   // STATS: same for phase B
+    unsigned long long pad[7];
+};
+
+struct __align__(128) Ctrl {
+    RoundCnt cnt[3];
+    // results (copied to the host after the run)
+    int32_t status;
+    int32_t pad1;
+    int64_t rounds;
+    int64_t tot_extracted, tot_edges, tot_succ, tot_inserts, tot_qscan, max_q, max_f, tot_dense;
+};
+
+// A sharded append list: segment s < kShards holds [s*cap, s*cap + min(count_s, cap)),
+// the spill segment [kShards*cap, ...).  Counters live 1 KB apart.
+template <typename T>
+struct Sharded {
+    T* base;
+    int32_t* cnt;       // cnt[s * kCntStride]
+    int64_t cap;        // per-shard capacity
+    int64_t spill_cap;  // capacity of the spill segment
+    int32_t* err;       // set to SSSP_ERR_INTERNAL if a reservation ever exceeded the spill
+    __device__ __forceinline__ T* seg(int s) const { return base + (int64_t)s * cap; }
+    __device__ __forceinline__ int64_t seg_count(int s) const {
+        const int64_t c = __ldcg(cnt + s * kCntStride);
+        return s < kShards ? (c < cap ? c : cap) : c;
+    }
+};
+
+struct RunParams {
+    int32_t n;
+    int32_t source;
+    int64_t m;
+    const int32_t* __restrict__ off;
+    const int32_t* __restrict__ idx;
+    const uint32_t* __restrict__ w;
+    uint64_t* dist;
+    int32_t* qbuf[2];   // queue storage, ping-pong
+    int64_t qcap;       // per-shard queue capacity
+    Desc* chunks;       // chunk descriptor storage
+    int64_t ccap;       // per-shard chunk capacity
+    int64_t cspill;     // chunk spill capacity
+    int32_t* counters;  // [3 slots][2 lists: queue, chunks][kSeg] * kCntStride
+    uint64_t* cta_min;  // [3 slots][kMaxCtas]: per-CTA min for Delta / Dijkstra
+    int64_t* cta_delta; // [3 slots][kMaxCtas]: per-CTA change of |Q| (inserts - extractions)
+    int64_t* cta_front; // [3 slots][kMaxCtas]: per-CTA (arcs << 32 | vertices) extracted
+    Desc* light;
+    uint64_t* samples;
+    Ctrl* ctrl;
+    uint64_t param;
+    uint32_t flags;
+    uint64_t seed;
+    int64_t max_rounds;
+    sssp_round* trace;
+    int64_t trace_cap;
+    int32_t* ext_count;
+    int32_t fuse_budget;  // fused vertices per warp per round (FUSE kernels)
+};
+
+__device__ __forceinline__ int32_t* counters_of(const RunParams& p, int slot, int list) {
+    return p.counters + (int64_t)((slot * 2 + list) * kSeg) * kCntStride;
+}
+__device__ __forceinline__ Sharded<int32_t> queue_of(const RunParams& p, int64_t round_of_queue) {
+    // Q_r lives in qbuf[r & 1]; its counts are in slot (r + 2) % 3
+    return Sharded<int32_t>{p.qbuf[round_of_queue & 1], counters_of(p, (int)((round_of_queue + 2) % 3), 0), p.qcap,
+                            (int64_t)p.n, &p.ctrl->status};
+}
+__device__ __forceinline__ Sharded<Desc> chunks_of(const RunParams& p, int64_t r) {
+    return Sharded<Desc>{p.chunks, counters_of(p, (int)(r % 3), 1), p.ccap, p.cspill, &p.ctrl->status};
+}
+
+__device__ __forceinline__ void reset_cnt(RoundCnt* c) {
+    c->nlight = 0;
+    c->nheavy = 0;
+    c->theta = 0;
+    c->fsize = 0;
+    c->edges = 0;
+    c->succ = 0;
+    c->inserts = 0;
+    c->split = 0;
+    c->busy_a = 0;
+    c->busy_b = 0;
+}
+
+__device__ __forceinline__ Desc ld_desc(const Desc* p) {
+    const uint4 v = __ldcg((const uint4*)p);
+    Desc e;
+    e.d = ((uint64_t)v.y << 32) | v.x;
+    e.beg = (int32_t)v.z;
+    e.len = (int32_t)v.w;
+    return e;
+}
+__device__ __forceinline__ void st_desc(Desc* p, uint64_t d, int32_t beg, int32_t len) {
+    __stcg((uint4*)p, make_uint4((uint32_t)d, (uint32_t)(d >> 32), (uint32_t)beg, (uint32_t)len));
+}
+__device__ __forceinline__ void st_desc_smem(Desc* p, uint64_t d, int32_t beg, int32_t len) {
+    p->d = d;
+    p->beg = beg;
+    p->len = len;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Global warp rank, CTA-minor: consecutive work items land on different SMs, so a
+// small round is spread over the whole GPU instead of the first few CTAs.
+__device__ __forceinline__ int64_t warp_rank() { return (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x; }
+
+// Filter read of delta[v] for a relaxation: through L1 (hub targets are shared by many
+// arcs of an SM).  A stale L1 copy can only be higher than the current value (delta only
+// decreases, and every grid barrier's fence invalidates L1), so it can only cause a CAS
+// that then fails and retries with the word the CAS returned: never a lost update.
+__device__ __forceinline__ uint64_t dist_filter_ld(const uint64_t* p) {
+    if (SSSP_L1DIST) return __ldca((const unsigned long long*)p);
+    return ld_cg_u64(p);
+}
+
+__host__ __device__ constexpr bool uses_min(int pol) {
+    return pol == SSSP_DELTA || pol == SSSP_DIJKSTRA || pol == SSSP_DELTA_STEPPING;
+}
+
+// --------------------------------------------------------------------- segment prefix
+// Exclusive prefix of a sharded list's segment counts, in shared memory (pref[kSeg] =
+// total).  Called by all threads; ends with __syncthreads.
+template <typename T>
+__device__ __forceinline__ void load_prefix(const Sharded<T>& L, int64_t* pref) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const int64_t c0 = L.seg_count(lane);                     // shards 0..31
+        const int64_t c1 = lane == 0 ? L.seg_count(kShards) : 0;  // spill
+        int64_t x = c0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t t = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += t;
+        }
+        const int64_t spill = __shfl_sync(kFull, c1, 0);
+        pref[lane] = x - c0;
+        if (lane == 31) {
+            pref[kShards] = x;
+            pref[kSeg] = x + spill;
+        }
+    }
+    __syncthreads();
+}
+static_assert(kShards == 32, "load_prefix assumes one warp of shards");
+
+// segment of virtual index i < total: largest s with pref[s] <= i (pref is smem)
+__device__ __forceinline__ int seg_of(const int64_t* pref, int64_t i) {
+    int s = 0;
+#pragma unroll
+    for (int step = 32; step > 0; step >>= 1)
+        if (s + step <= kShards && pref[s + step] <= i) s += step;
+    return s;
+}
+
+// --------------------------------------------------------------------- per-warp staging
+struct WarpStage {
+    int32_t take[kTBuf];  // ids that pass the theta test, extracted 32 at a time
+    int32_t q[kQBuf];     // ids appended to the next queue
+    uint64_t mins[32];    // bidirectional relaxation: per-vertex pulled minimum
+};
+struct FuseStage {        // FUSE kernels only (kept out of the others' shared memory, which is L1)
+    uint64_t fd[kFBuf];   // fused vertices: key ...
+    int32_t fid[kFBuf];   // ... and id
+};
+
+// dynamic shared memory: per-warp stages, theta samples, select scratch [, fuse stages]
+constexpr size_t kSmemBase = (kWarps * sizeof(WarpStage) + kSmemSamples * sizeof(uint64_t) + sizeof(SelectSmem) + 15) /
+                             16 * 16;
+
+struct Acc {
+    uint64_t minsucc = kInf;
+    uint32_t succ = 0;
+    uint32_t inserts = 0;
+    uint32_t fused = 0;        // STATS: vertices extracted by fusion
+    uint64_t fused_edges = 0;  // STATS: their arcs
+};
+
+struct Warp {  // per-warp working state (qn is warp-uniform)
+    WarpStage* st;
+    FuseStage* fs;
+    Sharded<int32_t> qnext;
+    RoundCnt* C;
+    uint64_t split;       // near/far split: keys <= split are held in the queue array
+    uint64_t fuse_theta;  // live rounds: theta (a vertex outside Q improved to <= theta is
+                          // extracted on the spot, DESIGN.md §5 "fusion"); 0 = no fusion
+    int64_t qdelta;       // this lane's inserts - extractions (|Q| bookkeeping)
+    uint64_t front;       // this lane's extractions: (arcs << 32) | vertices
+    int shard;
+    int32_t qn;
+    int32_t fn;       // staged fused vertices (warp-uniform)
+    int32_t fbudget;  // fusions left this round (warp-uniform)
+    Acc acc;
+};
+
+// A successful WriteMin replaced word w_old by value c (flag cleared).  Returns true iff
+// v must be appended to the near queue: it was outside Q (insertion) and c <= split, or
+// it was a far member of Q (value > split) that now falls into the near range.
+template <bool STATS>
+__device__ __forceinline__ bool admit(uint64_t w_old, uint64_t c, Warp& W) {
+    if (w_old & kTop) {
+        W.qdelta++;
+        if (STATS) W.acc.inserts++;
+        return c <= W.split;
+    }
+    return (w_old & kVal) > W.split && c <= W.split;
+}
+
+// Reserve `tot` slots of a sharded list for this warp (lane 0 does the atomics).
+// Element i < tot goes to p0 + i if i < fit, else to p1 + (i - fit) (spill segment).
+// The capacities make overflow impossible (a list never holds more than its bound), but a
+// reservation past the spill segment is still refused: `lim` < tot elements are writable
+// and the run fails with SSSP_ERR_INTERNAL instead of corrupting memory.
+template <typename T>
+__device__ __forceinline__ void reserve(const Sharded<T>& L, int shard, int32_t tot, T*& p0, int32_t& fit, T*& p1,
+                                        int32_t& lim) {
+    int64_t pos = 0, spos = 0;
+    if (lane_id() == 0) {
+        pos = atomicAdd(L.cnt + shard * kCntStride, tot);
+        const int64_t f = pos >= L.cap ? 0 : (L.cap - pos < tot ? L.cap - pos : tot);
+        if (f < tot) spos = atomicAdd(L.cnt + kShards * kCntStride, (int32_t)(tot - f));
+    }
+    pos = __shfl_sync(kFull, pos, 0);
+    spos = __shfl_sync(kFull, spos, 0);
+    fit = pos >= L.cap ? 0 : (int32_t)(L.cap - pos < tot ? L.cap - pos : tot);
+    const int64_t room = L.spill_cap - spos;
+    lim = fit + (int32_t)(room <= 0 ? 0 : (room < tot - fit ? room : tot - fit));
+    if (lim < tot && lane_id() == 0) atomicExch(L.err, (int32_t)SSSP_ERR_INTERNAL);
+    p0 = L.seg(shard) + pos;
+    p1 = L.seg(kShards) + spos;
+}
+
+__device__ __forceinline__ void wq_flush(Warp& W) {
+    if (W.qn == 0) return;
+    __syncwarp();
+    int32_t *p0, *p1;
+    int32_t fit, lim;
+    reserve(W.qnext, W.shard, W.qn, p0, fit, p1, lim);
+    for (int32_t i = lane_id(); i < lim; i += 32) {
+        const int32_t v = W.st->q[i];
+        if (i < fit)
+            p0[i] = v;
+        else
+            p1[i - fit] = v;
+    }
+    __syncwarp();
+    W.qn = 0;
+}
+
+// stage the lanes' ids with pred (one id per lane)
+__device__ __forceinline__ void wq_push1(Warp& W, bool pred, int32_t id) {
+    const uint32_t mask = __ballot_sync(kFull, pred);
+    if (!mask) return;
+    const int32_t cnt = __popc(mask);
+    if (W.qn + cnt > kQBuf) wq_flush(W);
+    if (pred) W.st->q[W.qn + __popc(mask & lanemask_lt())] = id;
+    W.qn += cnt;
+}
+
+// --------------------------------------------------------------------- relax
+// Outcome of a relaxation slot.
+enum { kNone = 0, kAppend = 1, kFused = 2 };
+
+// The word a successful WriteMin of c over word w writes: c with the flag cleared (v is
+// in Q), or - when fusing - c with the flag still set (v was outside Q and is extracted
+// on the spot by this warp, so it never enters Q).
+__device__ __forceinline__ bool fuses(bool fuse, uint64_t w, uint64_t c, const Warp& W) {
+    return fuse && (w & kTop) && c <= W.fuse_theta;
+}
+
+// WriteMin(delta[v], c) on the packed word, given a prior read `w`: CAS retries.
+template <int POL, bool STATS, bool FUSE, bool BIDIR>
+__device__ __forceinline__ int write_min(uint64_t* dist, int32_t v, uint64_t c, uint64_t w, bool fuse, Warp& W) {
+    while ((w & kVal) > c) {
+        const bool f = fuses(fuse, w, c, W);
+        const uint64_t old = atomicCAS((unsigned long long*)(dist + v), (unsigned long long)w,
+                                       (unsigned long long)(f ? (c | kTop) : c));
+        if (old == w) {
+            if (STATS) W.acc.succ++;
+            if (f) return kFused;
+            if (uses_min(POL)) W.acc.minsucc = c < W.acc.minsucc ? c : W.acc.minsucc;
+            return admit<STATS>(w, c, W) ? kAppend : kNone;
+        }
+        w = old;
+    }
+    return kNone;
+}
+
+// Relax kArcs arcs per lane (v < 0 = empty slot): filter loads, WriteMins, stage the
+// inserted ids (Alg. 1 lines 5-6).
+struct NoPull {
+    __device__ __forceinline__ void operator()(const int32_t (&)[kArcs], const uint64_t (&)[kArcs], uint64_t (&)[kArcs]) {}
+};
+
+template <int POL, bool STATS, bool FUSE, bool BIDIR, typename Pull = NoPull>
+__device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&v)[kArcs], uint64_t (&c)[kArcs],
+                                            Warp& W, Pull pull = Pull()) {
+    uint64_t cur[kArcs];
+#pragma unroll
+    for (int t = 0; t < kArcs; t++) cur[t] = v[t] >= 0 ? dist_filter_ld(p.dist + v[t]) : 0ull;
+    pull(v, cur, c);  // bidirectional relaxation may lower the candidates (SURVEY f-2)
+    // room for a full step of fusions and budget left (warp-uniform)
+    const bool fuse = FUSE && W.fuse_theta != 0 && W.fbudget > 0 && W.fn <= kFBuf - 32 * kArcs;
+    // first CAS attempt of every slot issued back to back (one round trip, not kArcs),
+    // then the rare retries
+    uint64_t old[kArcs];
+#pragma unroll
+    for (int t = 0; t < kArcs; t++)
+        old[t] = (v[t] >= 0 && (cur[t] & kVal) > c[t])
+                     ? atomicCAS((unsigned long long*)(p.dist + v[t]), (unsigned long long)cur[t],
+                                 (unsigned long long)(fuses(fuse, cur[t], c[t], W) ? (c[t] | kTop) : c[t]))
+                     : cur[t] + 1;  // "no attempt" marker: != cur[t]
+    int32_t cnt = 0, fcnt = 0;
+    int out[kArcs];
+#pragma unroll
+    for (int t = 0; t < kArcs; t++) {
+        out[t] = kNone;
+        if (v[t] >= 0 && (cur[t] & kVal) > c[t]) {
+            if (old[t] == cur[t]) {
+                if (STATS) W.acc.succ++;
+                if (fuses(fuse, cur[t], c[t], W)) {
+                    out[t] = kFused;
+                } else {
+                    if (uses_min(POL)) W.acc.minsucc = c[t] < W.acc.minsucc ? c[t] : W.acc.minsucc;
+                    out[t] = admit<STATS>(cur[t], c[t], W) ? kAppend : kNone;
+                }
+            } else {
+                out[t] = write_min<POL, STATS, FUSE, BIDIR>(p.dist, v[t], c[t], old[t], fuse, W);
+            }
+        }
+        cnt += out[t] == kAppend;
+        fcnt += out[t] == kFused;
+    }
+    if (__any_sync(kFull, cnt != 0)) {
+        const int32_t incl = warp_incl_scan(cnt);
+        const int32_t tot = __shfl_sync(kFull, incl, 31);
+        if (W.qn + tot > kQBuf) wq_flush(W);
+        int32_t pos = W.qn + incl - cnt;
+#pragma unroll
+        for (int t = 0; t < kArcs; t++)
+            if (out[t] == kAppend) W.st->q[pos++] = v[t];
+        W.qn += tot;
+    }
+    if (FUSE && fuse && __any_sync(kFull, fcnt != 0)) {
+        const int32_t incl = warp_incl_scan(fcnt);
+        const int32_t tot = __shfl_sync(kFull, incl, 31);
+        int32_t pos = W.fn + incl - fcnt;
+#pragma unroll
+        for (int t = 0; t < kArcs; t++)
+            if (out[t] == kFused) {
+                W.fs->fid[pos] = v[t];
+                W.fs->fd[pos] = c[t];
+                pos++;
+            }
+        W.fn += tot;
+        W.fbudget -= tot;
+    }
+}
+
+// One chunk: arcs [beg, beg+len) of a vertex with key d, len <= kChunk.  Lane-strided
+// so every load instruction of the warp reads 128 contiguous bytes.
+template <int POL, bool STATS, bool FUSE, bool BIDIR>
+__device__ __forceinline__ void relax_chunk(const RunParams& p, uint64_t d, int32_t beg, int32_t len, Warp& W) {
+    const int lane = lane_id();
+    int32_t v[kArcs];
+    uint64_t c[kArcs];
+#pragma unroll
+    for (int t = 0; t < kArcs; t++) {
+        const int32_t k = t * 32 + lane;
+        v[t] = k < len ? ld_stream_i32(p.idx + beg + k) : -1;
+        c[t] = d + (k < len ? ld_stream_u32(p.w + beg + k) : 0u);
+    }
+    relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W);
+}
+
+// Up to 32 vertices, one per lane (deg = 0 for none): the warp walks their
+// concatenated arc lists; arc e belongs to the largest lane o with excl[o] <= e.
+// Bidirectional relaxation (paper P:1360-1366, SURVEY f-2; undirected graphs only): the
+// keys gathered for the filter are the neighbours' tentative distances, so before
+// pushing, each vertex u of the step first pulls delta[u] <- min_v delta[v] + w(v,u) over
+// the step's arcs, lowers delta[u] (keeping its flag bit) and pushes with the lower key.
+struct BidirPull {
+    const RunParams* p;
+    uint64_t* mins;  // per-warp shared memory [32]
+    const int32_t* o;
+    const uint32_t* wt;
+    uint64_t* d;  // this lane's vertex key (updated)
+    int32_t uid;  // this lane's vertex id, -1 if none
+    __device__ __forceinline__ void operator()(const int32_t (&v)[kArcs], const uint64_t (&cur)[kArcs],
+                                               uint64_t (&c)[kArcs]) {
+        const int lane = lane_id();
+        mins[lane] = kInf;
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < kArcs; t++)
+            if (v[t] >= 0 && (cur[t] & kVal) != kVal)
+                atomicMin((unsigned long long*)(mins + o[t]), (unsigned long long)((cur[t] & kVal) + wt[t]));
+        __syncwarp();
+        const uint64_t best = mins[lane];
+        if (uid >= 0 && best < *d) {
+            uint64_t w = __ldcg((const unsigned long long*)(p->dist + uid));
+            while ((w & kVal) > best) {
+                const uint64_t old = atomicCAS((unsigned long long*)(p->dist + uid), (unsigned long long)w,
+                                               (unsigned long long)((w & kTop) | best));
+                if (old == w) {
+                    w = (w & kTop) | best;
+                    break;
+                }
+                w = old;
+            }
+            *d = (w & kVal) < best ? (w & kVal) : best;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < kArcs; t++) {
+            const uint64_t od = __shfl_sync(kFull, *d, o[t]);
+            if (v[t] >= 0) c[t] = od + wt[t];
+        }
+    }
+};
+
+template <int POL, bool STATS, bool FUSE, bool BIDIR>
+__device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, int32_t beg, int32_t deg, Warp& W,
+                                               int32_t uid = -1) {
+    const int lane = lane_id();
+    const int32_t incl = warp_incl_scan(deg);
+    const int32_t total = __shfl_sync(kFull, incl, 31);
+    const int32_t excl = incl - deg;
+    const int32_t rowbase = beg - excl;  // CSR position of concatenated arc e of this lane = rowbase + e
+    const bool bidir = BIDIR && __any_sync(kFull, uid >= 0);
+    for (int32_t s0 = 0; s0 < total; s0 += 32 * kArcs) {
+        int32_t v[kArcs], o[kArcs];
+        uint32_t wt[kArcs];
+        uint64_t c[kArcs];
+        // pull only into a vertex whose whole arc list is in this step: arcs pushed in an
+        // earlier step with a higher key would otherwise never see the lower one
+        const int32_t uid_step = (excl >= s0 && excl + deg <= s0 + 32 * kArcs) ? uid : -1;
+#pragma unroll
+        for (int t = 0; t < kArcs; t++) {
+            const int32_t e = s0 + t * 32 + lane;
+            o[t] = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int32_t x = __shfl_sync(kFull, excl, o[t] + step);
+                if (x <= e) o[t] += step;
+            }
+            const int32_t rb = __shfl_sync(kFull, rowbase, o[t]);
+            const uint64_t od = __shfl_sync(kFull, d, o[t]);
+            const bool ok = e < total;
+            v[t] = ok ? ld_stream_i32(p.idx + rb + e) : -1;
+            wt[t] = ok ? ld_stream_u32(p.w + rb + e) : 0u;
+            c[t] = od + wt[t];
+        }
+        if (BIDIR && bidir)
+            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, BidirPull{&p, W.st->mins, o, wt, &d, uid_step});
+        else
+            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W);
+    }
+}
+
+// Relax the fused vertices (already deleted from / never entered Q, key known), 32 at a
+// time from the top of the warp's stack; their relaxations may fuse more.
+template <int POL, bool STATS, bool FUSE, bool BIDIR>
+__device__ __forceinline__ void fuse_drain(const RunParams& p, Warp& W) {
+    if (!FUSE) return;
+    const int lane = lane_id();
+    while (W.fn > 0) {
+        const int32_t cnt = W.fn < 32 ? W.fn : 32;
+        __syncwarp();
+        int32_t id = -1;
+        uint64_t d = 0;
+        if (lane < cnt) {
+            id = W.fs->fid[W.fn - cnt + lane];
+            d = W.fs->fd[W.fn - cnt + lane];
+        }
+        __syncwarp();
+        W.fn -= cnt;
+        int32_t beg = 0, deg = 0;
+        if (id >= 0) {
+            beg = __ldg(p.off + id);
+            deg = __ldg(p.off + id + 1) - beg;
+        }
+        // a fused hub goes back to Q instead (its arcs belong in chunks, not in one warp)
+        bool back = false;
+        const int32_t hub = id;
+        if (id >= 0 && deg > kFuseMaxDeg) {
+            const uint64_t old = atomicCAS((unsigned long long*)(p.dist + id), (unsigned long long)(d | kTop),
+                                           (unsigned long long)d);
+            back = old == (d | kTop) && admit<STATS>(old, d, W);  // else a later WriteMin re-inserted it
+            id = -1;
+            deg = 0;
+        }
+        wq_push1(W, back, hub);
+        if (id >= 0) {
+            if (p.ext_count) atomicAdd(p.ext_count + id, 1);
+            W.front += 1 | ((uint64_t)deg << 32);
+            if (STATS) {
+                W.acc.fused++;  // counted as inserted and extracted (the |Q| identity holds)
+                W.acc.inserts++;
+                W.acc.fused_edges += (uint64_t)deg;
+            }
+        }
+        relax_vertices<POL, STATS, FUSE, BIDIR>(p, d, beg, deg, W, id);
+    }
+}
+
+// Cut the heavy lanes' vertices into kChunk-arc descriptors (one reservation per warp).
+__device__ __forceinline__ void emit_chunks(const Sharded<Desc>& CL, int shard, bool heavy, uint64_t d, int32_t beg,
+                                            int32_t deg, RoundCnt* C, bool stats) {
+    const uint32_t hm = __ballot_sync(kFull, heavy);
+    if (!hm) return;
+    const int lane = lane_id();
+    const int32_t nch = heavy ? (deg + kChunk - 1) / kChunk : 0;
+    const int32_t incl = warp_incl_scan(nch);
+    const int32_t tot = __shfl_sync(kFull, incl, 31);
+    const int32_t excl = incl - nch;
+    if (stats && lane == 0) atomicAdd(&C->nheavy, __popc(hm));
+    Desc *p0, *p1;
+    int32_t fit, lim;
+    reserve(CL, shard, tot, p0, fit, p1, lim);
+    for (int32_t j0 = 0; j0 < tot; j0 += 32) {
+        const int32_t j = j0 + lane;
+        int32_t o = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int32_t x = __shfl_sync(kFull, excl, o + step);
+            if (x <= j) o += step;
+        }
+        const int32_t ob = __shfl_sync(kFull, beg, o);
+        const int32_t oe = __shfl_sync(kFull, excl, o);
+        const int32_t od = __shfl_sync(kFull, deg, o);
+        const uint64_t odd = __shfl_sync(kFull, d, o);
+        if (j < lim) {
+            const int32_t k = (j - oe) * kChunk;
+            st_desc(j < fit ? p0 + j : p1 + (j - fit), odd, ob + k, min(kChunk, od - k));
+        }
+    }
+}
+
+// --------------------------------------------------------------------- phase A
+// Extract(theta) in two decoupled parts:
+//  scan:  kEnt queue entries per lane per step (all id loads, then all key gathers in
+//         flight); ids above theta are staged for the next queue, ids at or below it
+//         are staged in the warp's take buffer;
+//  batch: 32 staged ids at a time are deleted from Q (atomicOr, which returns the exact
+//         key they relax with), their CSR rows read, heavy ones cut into chunks and the
+//         light ones relaxed by the warp at once (live) or listed (snapshot).
+template <int POL, bool STATS, bool FUSE, bool BIDIR>
+__device__ __forceinline__ void take_batch(const RunParams& p, int32_t cnt, const Sharded<Desc>& CL, bool snap, Warp& W,
+                                           uint64_t& fs, uint64_t& edges) {
+    const int lane = lane_id();
+    __syncwarp();
+    int32_t id = lane < cnt ? W.st->take[lane] : -1;
+    uint64_t d = 0;
+    int32_t beg = 0, deg = 0;
+    if (id >= 0) {
+        const uint64_t old = atomicOr((unsigned long long*)(p.dist + id), (unsigned long long)kTop);  // delete from Q
+        d = old & kVal;
+        if (old & kTop) id = -1;  // already deleted by another copy (safety net: copies are not expected)
+    }
+    if (id >= 0) {
+        W.qdelta--;
+        W.front += 1;
+        beg = __ldg(p.off + id);
+        deg = __ldg(p.off + id + 1) - beg;
+        W.front += (uint64_t)deg << 32;
+        if (p.ext_count) atomicAdd(p.ext_count + id, 1);
+    }
+    if (STATS && id >= 0) {
+        fs += 1;
+        edges += (uint64_t)deg;
+    }
+    const bool heavy = deg > kLight;
+    const bool light = id >= 0 && deg > 0 && !heavy;
+    emit_chunks(CL, W.shard, heavy, d, beg, deg, W.C, STATS);
+    if (snap) {
+        const int32_t ls = warp_append_slot(light, &W.C->nlight);
+        if (light) st_desc(p.light + ls, d, beg, deg);
+    } else if (__any_sync(kFull, light)) {
+        relax_vertices<POL, STATS, FUSE, BIDIR>(p, d, beg, light ? deg : 0, W, light ? id : -1);
+    }
+}
+
+template <int POL, bool STATS, bool FUSE, bool BIDIR>
+__device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_t>& QC, const int64_t* qpref,
+                                        const Sharded<Desc>& CL, uint64_t theta, bool snap, uint64_t& minrem, Warp& W) {
+    const int lane = lane_id();
+    const int64_t q = qpref[kSeg];
+    const int64_t gw = warp_rank();
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    uint64_t fs = 0, edges = 0;
+    int32_t tn = 0;  // staged take ids (warp-uniform)
+    // kEnt entries per lane only when every warp gets at least two such steps; small
+    // queues are spread one entry per lane so that more warps share the round
+    const int ent = q >= nwarps * (32 * kEnt) ? kEnt : 1;
+    // Small queues: an equal contiguous share per warp (+-1 entry).  A round lasts as long
+    // as its slowest warp; strided tiles left some warps with 3 tiles and others with 1,
+    // and contiguous ids (appended together) keep a warp's fusion local.  Large queues:
+    // strided tiles, since ids appended together carry correlated work (R-MAT hubs).
+    const bool contig = q < (int64_t)kContigTiles * 32 * nwarps;
+    const int64_t lo = contig ? gw * q / nwarps : gw * (32 * ent);
+    const int64_t hi = contig ? (gw + 1) * q / nwarps : q;
+    const int64_t stride = contig ? 32 * ent : nwarps * (32 * ent);
+    for (int64_t base = lo; base < hi; base += stride) {
+        int32_t id[kEnt];
+        uint64_t val[kEnt];
+        const int sg = seg_of(qpref, base);  // warp-uniform
+#pragma unroll
+        for (int e = 0; e < kEnt; e++) {
+            const int64_t i = base + e * 32 + lane;
+            id[e] = -1;
+            if (e < ent && i < hi) {
+                int s = sg;
+                while (qpref[s + 1] <= i) s++;
+                id[e] = ld_cg_i32(QC.seg(s) + (i - qpref[s]));
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < kEnt; e++) val[e] = id[e] >= 0 ? (ld_cg_u64(p.dist + id[e]) & kVal) : kVal;
+#pragma unroll
+        for (int e = 0; e < kEnt; e++) {
+            const bool take = id[e] >= 0 && val[e] <= theta;
+            const bool rem = id[e] >= 0 && !take;
+            wq_push1(W, rem && val[e] <= W.split, id[e]);  // above the split: stays in Q as a far member
+            if (uses_min(POL) && rem) minrem = val[e] < minrem ? val[e] : minrem;
+            const uint32_t tm = __ballot_sync(kFull, take);
+            if (take) W.st->take[tn + __popc(tm & lanemask_lt())] = id[e];
+            tn += __popc(tm);
+        }
+        int32_t done = 0;
+        while (tn - done >= 32) {
+            if (done) {  // move the next 32 to the front (take_batch reads take[0..32))
+                __syncwarp();
+                const int32_t x = W.st->take[done + lane];
+                __syncwarp();
+                W.st->take[lane] = x;
+            }
+            take_batch<POL, STATS, FUSE, BIDIR>(p, 32, CL, snap, W, fs, edges);
+            done += 32;
+        }
+        if (done) {  // keep the remainder (< 32) at the front
+            __syncwarp();
+            const bool mv = lane < tn - done;
+            int32_t x = 0;
+            if (mv) x = W.st->take[done + lane];
+            __syncwarp();
+            if (mv) W.st->take[lane] = x;
+            tn -= done;
+        }
+    }
+    if (tn) take_batch<POL, STATS, FUSE, BIDIR>(p, tn, CL, snap, W, fs, edges);
+    fuse_drain<POL, STATS, FUSE, BIDIR>(p, W);
+    if (STATS) {
+        fs = warp_sum(fs);
+        edges = warp_sum(edges);
+        if (lane == 0 && fs) atomicAdd(&W.C->fsize, (unsigned long long)fs);
+        if (lane == 0 && edges) atomicAdd(&W.C->edges, (unsigned long long)edges);
+    }
+}
+
+// --------------------------------------------------------------------- phase B
+template <int POL, bool STATS, bool FUSE, bool BIDIR>
+__device__ __forceinline__ void phase_b(const RunParams& p, const Sharded<Desc>& CL, const int64_t* cpref, int32_t nl,
+                                        Warp& W) {
+    const int lane = lane_id();
+    const int64_t gw = warp_rank();
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nb = ((int64_t)nl + 31) / 32;
+    const int64_t nc = cpref[kSeg];
+    const int64_t total = nb + nc;
+    auto chunk_at = [&](int64_t i) {  // i-th descriptor of the concatenated segments
+        const int s = seg_of(cpref, i);
+        return ld_desc(CL.seg(s) + (i - cpref[s]));
+    };
+    int64_t item = gw;
+    Desc nxt;
+    if (item >= nb && item < total) nxt = chunk_at(item - nb);
+    for (; item < total; item += nwarps) {
+        if (item < nb) {
+            const int64_t j = item * 32 + lane;
+            Desc e;
+            if (j < nl) {
+                e = ld_desc(p.light + j);
+            } else {
+                e.d = 0;
+                e.beg = 0;
+                e.len = 0;
+            }
+            relax_vertices<POL, STATS, FUSE, BIDIR>(p, e.d, e.beg, e.len, W);
+            if (item + nwarps >= nb && item + nwarps < total) nxt = chunk_at(item + nwarps - nb);
+        } else {
+            const Desc e = nxt;
+            if (item + nwarps < total) nxt = chunk_at(item + nwarps - nb);  // prefetch
+            relax_chunk<POL, STATS, FUSE, BIDIR>(p, e.d, e.beg, e.len, W);
+            if (FUSE && W.fn > kFBuf - 32 * kArcs) fuse_drain<POL, STATS, FUSE, BIDIR>(p, W);
+        }
+    }
+    fuse_drain<POL, STATS, FUSE, BIDIR>(p, W);
+}
+
+template <int POL, bool STATS, bool FUSE, bool BIDIR>
+__device__ __forceinline__ void flush_acc(const RunParams& p, int64_t r, Warp& W) {
+    wq_flush(W);
+    const int64_t dq = warp_sum(W.qdelta);
+    if (lane_id() == 0 && dq) atomicAdd((unsigned long long*)(p.cta_delta + (r % 3) * kMaxCtas + blockIdx.x),
+                                        (unsigned long long)dq);
+    W.qdelta = 0;
+    const uint64_t fr = warp_sum(W.front);
+    if (lane_id() == 0 && fr) atomicAdd((unsigned long long*)(p.cta_front + (r % 3) * kMaxCtas + blockIdx.x),
+                                        (unsigned long long)fr);
+    W.front = 0;
+    if (STATS) {
+        const uint32_t s = warp_sum(W.acc.succ), ins = warp_sum(W.acc.inserts), fu = warp_sum(W.acc.fused);
+        const uint64_t fe = warp_sum(W.acc.fused_edges);
+        if (lane_id() == 0 && s) atomicAdd(&W.C->succ, (unsigned long long)s);
+        if (lane_id() == 0 && ins) atomicAdd(&W.C->inserts, (unsigned long long)ins);
+        if (lane_id() == 0 && fu) atomicAdd(&W.C->fsize, (unsigned long long)fu);
+        if (lane_id() == 0 && fe) atomicAdd(&W.C->edges, (unsigned long long)fe);
+    }
+    W.acc.succ = 0;
+    W.acc.inserts = 0;
+    W.acc.fused = 0;
+    W.acc.fused_edges = 0;
+}
+
+// --------------------------------------------------------------------- ExtDist for rho
+struct SmemKey {
+    const uint64_t* a;
+    __device__ uint64_t operator()(int64_t i) const { return a[i]; }
+};
+struct QueueVal {  // value of the i-th queued id (flag bit masked off), read through L2
+    Sharded<int32_t> Q;
+    const int64_t* pref;
+    const uint64_t* dist;
+    __device__ uint64_t operator()(int64_t i) const {
+        const int s = seg_of(pref, i);
+        return ld_cg_u64(dist + ld_cg_i32(Q.seg(s) + (i - pref[s]))) & kVal;
+    }
+};
+
+__device__ __forceinline__ uint64_t sample_index(uint64_t seed, int64_t round, uint64_t j, uint64_t q) {
+    return splitmix64(seed ^ splitmix64(((uint64_t)round << 32) | j)) % q;
+}
+
+// k-th smallest (1-based) of s <= blockDim keys in shared memory by rank counting:
+// the key x with #{< x} < k <= #{<= x}.  One pass of broadcast reads, two barriers.
+__device__ __forceinline__ uint64_t cta_kth_by_rank(const uint64_t* keys, int s, uint64_t k, SelectSmem& sm) {
+    const int tid = threadIdx.x;
+    if (tid < s) {
+        const uint64_t x = keys[tid];
+        uint32_t lt = 0, le = 0;
+        int j = 0;
+        for (; j + 8 <= s; j += 8) {  // 8 independent broadcast loads in flight
+            uint64_t y[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) y[u] = keys[j + u];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                lt += y[u] < x;
+                le += y[u] <= x;
+            }
+        }
+        for (; j < s; j++) {
+            const uint64_t y = keys[j];
+            lt += y < x;
+            le += y <= x;
+        }
+        if (lt < k && k <= le) sm.bcast[0] = x;  // every writer writes the same value
+    }
+    __syncthreads();
+    const uint64_t th = sm.bcast[0];
+    __syncthreads();
+    return th;
+}
+
+// --------------------------------------------------------------------- near/far queue
+// The queue array holds only the NEAR members of Q (key <= split); FAR members (key >
+// split) are implicit: their flag bit says "in Q" and nothing else lists them.  When the
+// near part runs low, a coalesced dense pass over delta moves the FAR keys in (split,
+// split'] into the queue (DESIGN.md §5 "near/far").  Rounds then rescan ~kNearK rounds
+// of work instead of all of Q.
+
+// Dense pass: append every far member with value in (lo, hi] to the list L (staged).
+__device__ __forceinline__ void far_to_near(const RunParams& p, const Sharded<int32_t>& L, uint64_t lo, uint64_t hi,
+                                            Warp& W) {
+    const int lane = lane_id();
+    const Sharded<int32_t> saved = W.qnext;
+    W.qnext = L;
+    const int64_t gw = warp_rank();
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    constexpr int kV = 8;
+    for (int64_t base = gw * (32 * kV); base < p.n; base += nwarps * (32 * kV)) {
+        uint64_t x[kV];
+#pragma unroll
+        for (int t = 0; t < kV; t++) {
+            const int64_t v = base + t * 32 + lane;
+            x[t] = v < p.n ? __ldcg((const unsigned long long*)(p.dist + v)) : kInf;
+        }
+#pragma unroll
+        for (int t = 0; t < kV; t++) {
+            const uint64_t val = x[t] & kVal;
+            wq_push1(W, !(x[t] & kTop) && val > lo && val <= hi, (int32_t)(base + t * 32 + lane));
+        }
+    }
+    wq_flush(W);
+    W.qnext = saved;
+}
+
+// CTA-0 estimate of the value below which about `want` far members lie: rejection-sample
+// vertices, keep the far ones, take the matching order statistic (kInf if none seen).
+static __device__ __forceinline__ uint64_t far_quantile(const RunParams& p, uint64_t split, int64_t far, int64_t want, int64_t r,
+                                 uint64_t* keys, SelectSmem& sm, int32_t* cnt) {
+    if (threadIdx.x == 0) *cnt = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < kFarSamples; j += blockDim.x) {
+        const uint64_t v = splitmix64(p.seed ^ 0xF00DF00DF00DULL ^ splitmix64(((uint64_t)r << 32) | (uint64_t)j)) %
+                           (uint64_t)p.n;
+        const uint64_t x = __ldcg((const unsigned long long*)(p.dist + v));
+        if (!(x & kTop) && (x & kVal) > split) keys[atomicAdd(cnt, 1)] = x & kVal;
+    }
+    __syncthreads();
+    const int32_t h = *cnt;
+    if (h == 0) return kInf;
+    uint64_t k = (uint64_t)(((double)want / (double)far) * h) + 1;
+    k = k > (uint64_t)h ? (uint64_t)h : k;
+    return h <= kRankSelect ? cta_kth_by_rank(keys, h, k, sm) : cta_kth_smallest(SmemKey{keys}, h, k, sm);
+}
+
+// --------------------------------------------------------------------- the round loop
+template <int POL, bool STATS, bool FUSE, bool BIDIR>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpStage* stage = (WarpStage*)smem_raw;                                // [kWarps]
+    uint64_t* s_keys = (uint64_t*)(smem_raw + kWarps * sizeof(WarpStage));  // [kSmemSamples]
+    SelectSmem& sm = *(SelectSmem*)(s_keys + kSmemSamples);
+    FuseStage* fstage = (FuseStage*)(smem_raw + kSmemBase);                  // [kWarps], FUSE only
+    __shared__ int64_t qpref[kSeg + 1];  // segment prefix of Q_r's near part
+    __shared__ int64_t cpref[kSeg + 1];  // segment prefix of the round's chunk list
+    __shared__ uint64_t bc_u[3];         // min_Q (Delta / Dijkstra), CTA-0 theta, CTA-0 split
+    __shared__ int64_t bc_dq;
+    __shared__ uint64_t bc_front;
+    __shared__ int32_t bc_nl, bc_cnt;
+    __shared__ uint64_t red[kWarps];
+    Ctrl* ctrl = p.ctrl;
+    Warp W;
+    W.st = stage + (threadIdx.x >> 5);
+    W.fs = fstage + (threadIdx.x >> 5);
+    W.shard = (int)(warp_rank() % kShards);
+    W.qn = 0;
+    W.fn = 0;
+    W.qdelta = 0;
+    W.front = 0;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
+
+    // Alg. 1 lines 1-2: delta[.] = +inf (not in Q), delta[s] = 0 (in Q), Q_1 = {s}
+    for (int64_t i = gtid; i < p.n; i += gsize) p.dist[i] = (i == p.source) ? 0ull : kInf;
+    if (p.ext_count)
+        for (int64_t i = gtid; i < p.n; i += gsize) p.ext_count[i] = 0;
+    for (int64_t i = gtid; i < 3 * 2 * kSeg; i += gsize) p.counters[i * kCntStride] = 0;
+    for (int64_t i = gtid; i < 3 * kMaxCtas; i += gsize) {
+        p.cta_min[i] = kInf;
+        p.cta_delta[i] = 0;
+        p.cta_front[i] = 0;
+    }
+    if (gtid == 0) {
+        p.qbuf[1][0] = p.source;  // Q_1 lives in qbuf[1], shard 0
+        for (int c = 0; c < 3; c++) reset_cnt(&ctrl->cnt[c]);
+        ctrl->status = 0;
+        ctrl->rounds = 0;
+        ctrl->tot_extracted = ctrl->tot_edges = ctrl->tot_succ = ctrl->tot_inserts = 0;
+        ctrl->tot_qscan = ctrl->max_q = ctrl->max_f = 0;
+        ctrl->tot_dense = 0;
+    }
+    grid_sync(nullptr);
+    if (gtid == 0) {
+        p.counters[0] = 1;  // |Q_1| = 1 (slot 0, queue list, shard 0)
+        p.cta_min[0] = 0;   // min_Q delta = delta[s] = 0
+    }
+    grid_sync(nullptr);
+
+    // near/far queue for rho only (Delta* / BF / Dijkstra keep split = +inf: all of Q listed)
+    const bool nearfar = POL == SSSP_RHO && !(p.flags & SSSP_RUN_NO_NEARFAR);
+    uint64_t split = kInf;  // near/far split (uniform across the grid)
+    int64_t qtot = 1;       // |Q_r| = near + far
+    uint64_t theta_prev = 0;
+    int warm = 0;
+    int64_t r = 1;
+    for (;; r++) {
+        RoundCnt* C = &ctrl->cnt[r % 3];
+        const Sharded<int32_t> QC = queue_of(p, r);
+        const Sharded<Desc> CL = chunks_of(p, r);
+        // |Q_r| = |Q_{r-1}| + sum over CTAs of (inserts - extractions) in round r-1
+        if ((threadIdx.x >> 5) == 2 && r > 1) {  // warp 2: the previous round's frontier size and arcs
+            const int lane = lane_id();
+            const int64_t* cf = p.cta_front + ((r + 2) % 3) * kMaxCtas;
+            uint64_t sf = 0;
+            for (int i = lane; i < (int)gridDim.x; i += 32) sf += __ldcg((const unsigned long long*)(cf + i));
+            sf = warp_sum(sf);
+            if (lane == 0) bc_front = sf;
+        }
+        if ((threadIdx.x >> 5) == 1 && r > 1) {  // warp 1, in parallel with warp 0's load_prefix
+            const int lane = lane_id();
+            const int64_t* cd = p.cta_delta + ((r + 2) % 3) * kMaxCtas;
+            int64_t sdq = 0;
+            for (int i = lane; i < (int)gridDim.x; i += 32) sdq += __ldcg((const long long*)(cd + i));
+            sdq = warp_sum(sdq);
+            if (lane == 0) bc_dq = sdq;
+        }
+        load_prefix(QC, qpref);  // ends with __syncthreads
+        if (r > 1) qtot += bc_dq;
+        int64_t qn = qpref[kSeg];  // near part of Q_r
+        if (qtot == 0) break;      // while |Q| > 0
+        if (r > p.max_rounds) {
+            if (gtid == 0) ctrl->status = SSSP_ERR_ROUNDS;
+            break;
+        }
+        uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+        int64_t dense = 0;
+        if (STATS && gtid == 0) t0 = globaltimer();
+        if (gtid == 0) reset_cnt(&ctrl->cnt[(r + 1) % 3]);
+        if (gtid < 2 * kSeg) {  // counters of slot (r+1)%3: written in round r+1, read in r+1 / r+2
+            p.counters[((int64_t)(((r + 1) % 3) * 2) * kSeg + gtid) * kCntStride] = 0;
+        }
+        if (threadIdx.x == 0) {
+            p.cta_delta[((r + 1) % 3) * kMaxCtas + blockIdx.x] = 0;
+            p.cta_front[((r + 1) % 3) * kMaxCtas + blockIdx.x] = 0;
+        }
+        W.qnext = queue_of(p, r + 1);
+        W.C = C;
+
+        // ---- ExtDist (Table tab:framework) and near/far maintenance
+        uint64_t theta;
+        // A round that lowers the split runs snapshot-style (Extract finishes before any
+        // relax): a live relax could not tell a near id still listed from one Extract
+        // just moved to the far part (DESIGN.md §5 near/far).
+        bool snap = (p.flags & SSSP_RUN_SNAPSHOT) != 0;
+        if (POL == SSSP_BELLMAN_FORD) {
+            theta = kInf;
+        } else if (POL == SSSP_DIJKSTRA || POL == SSSP_DELTA || POL == SSSP_DELTA_STEPPING) {
+            // min_Q delta = min over the per-CTA minima of the previous round
+            if (threadIdx.x < 32) {
+                const uint64_t* cm = p.cta_min + ((r + 2) % 3) * kMaxCtas;
+                uint64_t mn = kInf;
+                for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) {
+                    const uint64_t x = __ldcg((const unsigned long long*)(cm + i));
+                    mn = x < mn ? x : mn;
+                }
+                mn = warp_min_u64(mn);
+                if (threadIdx.x == 0) bc_u[0] = mn;
+            }
+            __syncthreads();
+            const uint64_t minq = bc_u[0];  // <= min_{v in Q} delta[v] (exact in snapshot mode)
+            if (POL == SSSP_DIJKSTRA) {
+                theta = minq;
+            } else if (POL == SSSP_DELTA_STEPPING && r > 1 && minq <= theta_prev) {
+                theta = theta_prev;  // FinishCheck failed: Bellman-Ford substep on the same bucket (R19)
+            } else {
+                const uint64_t D = p.param;  // theta_i = i*Delta, skipping empty steps (reading R2)
+                const uint64_t x = theta_prev > kInf - D ? kInf : theta_prev + D;
+                const uint64_t y = (minq / D + (minq % D != 0)) * D;
+                theta = x > y ? x : y;
+                theta_prev = theta;
+            }
+        } else {  // rho
+            uint64_t rho = p.param;
+            if (!(p.flags & SSSP_RUN_NO_WARMUP) && (uint64_t)qtot > rho && warm < 2) {
+                warm++;
+                rho = rho / 10 ? rho / 10 : 1;  // reading R7
+            }
+            const uint64_t want = rho > kInf / (4 * kNearK) ? kInf / 4 : (uint64_t)kNearK * rho;
+            // pull far keys in until the near part holds the rho smallest of Q (or all of Q)
+            for (int it = 0; nearfar && qtot > qn && ((uint64_t)qtot <= rho || (uint64_t)qn < rho); it++) {
+                uint64_t hi = kInf;
+                if ((uint64_t)qtot > rho && it < 3) {
+                    if (blockIdx.x == 0) {
+                        const uint64_t tgt = want > kInf >> 4 ? want : want << it;
+                        int64_t need = tgt >= (uint64_t)qtot ? qtot : (int64_t)tgt - qn;
+                        need = need < 1 ? 1 : need;
+                        const uint64_t h = need >= qtot - qn ? kInf
+                                                             : far_quantile(p, split, qtot - qn, need, r * 4 + it,
+                                                                            s_keys, sm, &bc_cnt);
+                        if (threadIdx.x == 0) C->split = h;
+                    }
+                    grid_sync(nullptr);
+                    if (threadIdx.x == 0) bc_u[2] = __ldcg((const unsigned long long*)&C->split);
+                    __syncthreads();
+                    hi = bc_u[2];
+                }
+                far_to_near(p, QC, split, hi, W);
+                dense += p.n;
+                grid_sync(nullptr);
+                load_prefix(QC, qpref);
+                qn = qpref[kSeg];
+                split = hi;
+            }
+            const QueueVal qv{QC, qpref, p.dist};
+            if (nearfar && (uint64_t)qn > 4 * want && qn > (int64_t)(p.n >> 5)) {
+                // the near part grew far beyond the target: lower the split to about the
+                // want-th smallest near key (CTA 0 + broadcast keeps it grid-uniform);
+                // Extract then leaves the near ids above it to the far part
+                if (blockIdx.x == 0) {
+                    uint64_t s2 = sample_count((uint64_t)qn, want);
+                    s2 = s2 > (uint64_t)kSmemSamples ? (uint64_t)kSmemSamples : s2;
+                    for (uint64_t j = threadIdx.x; j < s2; j += blockDim.x)
+                        s_keys[j] = qv((int64_t)sample_index(p.seed ^ 0x5EED5EEDull, r, j, (uint64_t)qn));
+                    __syncthreads();
+                    uint64_t k = (want * s2 + (uint64_t)qn - 1) / (uint64_t)qn;
+                    k = k < 1 ? 1 : (k > s2 ? s2 : k);
+                    const uint64_t h = cta_kth_smallest(SmemKey{s_keys}, (int64_t)s2, k, sm);
+                    if (threadIdx.x == 0) C->split = h;
+                }
+                grid_sync(nullptr);
+                if (threadIdx.x == 0) bc_u[2] = __ldcg((const unsigned long long*)&C->split);
+                __syncthreads();
+                if (bc_u[2] < split) {
+                    split = bc_u[2];
+                    snap = true;
+                }
+            }
+            const uint64_t s = sample_count((uint64_t)qn, rho);
+            if ((uint64_t)qtot <= rho) {
+                theta = kInf;  // |Q| <= rho: extract all
+            } else if ((uint64_t)qn < rho) {
+                theta = split;  // (near part short of rho after the pulls: extract all of it)
+            } else if (!(p.flags & SSSP_RUN_RHO_EXACT) && s <= (uint64_t)kSmemSamples) {
+                // every CTA draws the same samples of the near part (which holds the rho
+                // smallest keys of Q) and selects the same theta: no barrier
+                for (uint64_t j = threadIdx.x; j < s; j += blockDim.x)
+                    s_keys[j] = qv((int64_t)sample_index(p.seed, r, j, (uint64_t)qn));
+                __syncthreads();
+                uint64_t k = (rho * s + (uint64_t)qn - 1) / (uint64_t)qn;
+                k = k < 1 ? 1 : (k > s ? s : k);
+                theta = s <= (uint64_t)kRankSelect ? cta_kth_by_rank(s_keys, (int)s, k, sm)
+                                                   : cta_kth_smallest(SmemKey{s_keys}, (int64_t)s, k, sm);
+            } else {
+                if (blockIdx.x == 0) {
+                    uint64_t th;
+                    if (p.flags & SSSP_RUN_RHO_EXACT) {
+                        th = cta_kth_smallest(qv, qn, rho, sm);
+                    } else {
+                        for (uint64_t j = threadIdx.x; j < s; j += blockDim.x)
+                            p.samples[j] = qv((int64_t)sample_index(p.seed, r, j, (uint64_t)qn));
+                        __syncthreads();
+                        uint64_t k = (rho * s + (uint64_t)qn - 1) / (uint64_t)qn;
+                        k = k < 1 ? 1 : (k > s ? s : k);
+                        th = cta_kth_smallest(ArrayKey{p.samples}, (int64_t)s, k, sm);
+                    }
+                    if (threadIdx.x == 0) C->theta = th;
+                }
+                grid_sync(nullptr);
+                if (threadIdx.x == 0) bc_u[1] = __ldcg((const unsigned long long*)&C->theta);
+                __syncthreads();
+                theta = bc_u[1];
+            }
+        }
+        W.split = split;
+        // fusion in live rounds that are sparse: a sparse graph, or a previous frontier that
+        // averaged fewer than 20 arcs per vertex (the paper's rule)
+        const uint64_t fv = r > 1 ? (bc_front & 0xFFFFFFFFull) : 1, fe = r > 1 ? (bc_front >> 32) : 0;
+        const bool sparse = p.m < (int64_t)kSparseDeg * p.n || fe < (uint64_t)kSparseDeg * fv;
+        W.fuse_theta = (snap || !sparse) ? 0 : theta;
+        W.fbudget = p.fuse_budget;
+        if (STATS && gtid == 0) t1 = globaltimer();
+
+        // ---- phase A: Extract(theta) (+ light relax in live mode)
+        uint64_t minrem = kInf;
+        const uint64_t ta = STATS ? globaltimer() : 0;
+        phase_a<POL, STATS, FUSE, BIDIR>(p, QC, qpref, CL, theta, snap, minrem, W);
+        if (STATS && lane_id() == 0) atomicAdd(&C->busy_a, (unsigned long long)(globaltimer() - ta));
+        flush_acc<POL, STATS, FUSE, BIDIR>(p, r, W);
+        grid_sync(nullptr);
+        if (STATS && gtid == 0) t2 = globaltimer();
+        // ---- phase B: heavy chunks (+ light list in snapshot mode)
+        load_prefix(CL, cpref);
+        if (threadIdx.x == 0) bc_nl = snap ? __ldcg(&C->nlight) : 0;
+        __syncthreads();
+        const int32_t nl = bc_nl;
+        const bool phase_b_work = cpref[kSeg] + nl > 0;
+        if (phase_b_work) {
+            const uint64_t tb = STATS ? globaltimer() : 0;
+            phase_b<POL, STATS, FUSE, BIDIR>(p, CL, cpref, nl, W);
+            if (STATS && lane_id() == 0) atomicAdd(&C->busy_b, (unsigned long long)(globaltimer() - tb));
+        }
+        if (uses_min(POL)) {  // this CTA's min over kept ids and successful WriteMins
+            uint64_t mn = warp_min_u64(minrem < W.acc.minsucc ? minrem : W.acc.minsucc);
+            if (lane_id() == 0) red[threadIdx.x >> 5] = mn;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int i = 1; i < kWarps; i++) mn = red[i] < mn ? red[i] : mn;
+                p.cta_min[(r % 3) * kMaxCtas + blockIdx.x] = mn;
+            }
+            W.acc.minsucc = kInf;
+        }
+        if (phase_b_work) {
+            flush_acc<POL, STATS, FUSE, BIDIR>(p, r, W);
+            grid_sync(nullptr);
+        } else if (uses_min(POL) || STATS) {
+            grid_sync(nullptr);
+        }
+        if (STATS && gtid == 0) t3 = globaltimer();
+
+        if (STATS && gtid == 0) {
+            const int64_t f = (int64_t)C->fsize;
+            if (p.trace && r - 1 < p.trace_cap) {
+                sssp_round* t = p.trace + (r - 1);
+                t->qsize = qtot;
+                t->fsize = f;
+                t->edges = (int64_t)C->edges;
+                t->inserts = (int64_t)C->inserts;
+                t->succ = (int64_t)C->succ;
+                t->theta = theta;
+                t->nheavy = (int64_t)C->nheavy;
+                t->t_theta_ns = (int64_t)(t1 - t0);
+                t->t_extract_ns = (int64_t)(t2 - t1);
+                t->t_relax_ns = (int64_t)(t3 - t2);
+                t->qnear = qn;
+                t->dense = dense;
+                t->busy_a_ns = (int64_t)C->busy_a;
+                t->busy_b_ns = (int64_t)C->busy_b;
+            }
+            ctrl->tot_extracted += f;
+            ctrl->tot_edges += (int64_t)C->edges;
+            ctrl->tot_succ += (int64_t)C->succ;
+            ctrl->tot_inserts += (int64_t)C->inserts;
+            ctrl->tot_qscan += qn;
+            ctrl->tot_dense += dense;
+            ctrl->max_q = qtot > ctrl->max_q ? qtot : ctrl->max_q;
+            ctrl->max_f = f > ctrl->max_f ? f : ctrl->max_f;
+        }
+    }
+    if (gtid == 0) ctrl->rounds = r - 1;
+    // S6 output: strip the flag bit (every reached vertex was extracted; INF stays INF)
+    for (int64_t i = gtid; i < p.n; i += gsize) {
+        const uint64_t x = __ldcg((const unsigned long long*)(p.dist + i));
+        if (x != kInf && (x & kTop)) p.dist[i] = x & kVal;
+    }
+}
+
+typedef void (*KernelFn)(RunParams);
+
+constexpr size_t smem_bytes(bool fuse) { return kSmemBase + (fuse ? kWarps * sizeof(FuseStage) : 0); }
+
+// Kernel tables, one per (policy, bidirectional) object file (inst.cu); mode bit 0 = fusion.
+#define SSSP_DECLARE_TABLE(P, B) KernelFn kernel_table_##P##_##B(bool stats, bool fuse);
+SSSP_DECLARE_TABLE(0, 0) SSSP_DECLARE_TABLE(0, 1) SSSP_DECLARE_TABLE(1, 0) SSSP_DECLARE_TABLE(1, 1)
+SSSP_DECLARE_TABLE(2, 0) SSSP_DECLARE_TABLE(2, 1) SSSP_DECLARE_TABLE(3, 0) SSSP_DECLARE_TABLE(3, 1)
+SSSP_DECLARE_TABLE(4, 0) SSSP_DECLARE_TABLE(4, 1)
+#undef SSSP_DECLARE_TABLE
+
+}  // namespace sssp

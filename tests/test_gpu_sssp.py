@@ -261,3 +261,18 @@ def test_fusion_variants(cuda_device):
         r0 = h.last_stats["rounds"]
         h.run(g.source, "rho", 64, fuse_budget=4096)
         assert h.last_stats["rounds"] < r0
+
+
+def test_bidirectional_undirected(cuda_device):
+    """Bidirectional relaxation (SURVEY f-2) on undirected graphs: exact
+    distances for every policy and mode, including fusion and snapshot rounds."""
+    P = _P()
+    graphs = [gen.make(n) for n in ("grid64", "rmat12", "rgg64k", "rmat14log")]
+    graphs += [g for g in rng_graphs(30, seed0=505, nmax=2000, directed=False)]
+    for g in graphs:
+        want = oracle.dijkstra(g)
+        h = P.SSSP.from_graph(g)
+        for pol, par in (("rho", 2), ("rho", 256), ("delta", 1000), ("delta_stepping", 1000), ("bellman_ford", 0),
+                         ("dijkstra", 0)):
+            for kw in (dict(), dict(snapshot=True), dict(fuse=False)):
+                _assert_same(_run(h, g, pol, par, bidir=True, **kw), want, f"{g.name}/{pol}/{par}/{kw}/bidir")
