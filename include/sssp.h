@@ -174,6 +174,18 @@ sssp_status sssp_run_ex(sssp_handle *h, int32_t source, sssp_policy policy, uint
 sssp_status sssp_run_host(sssp_handle *h, int32_t source, sssp_policy policy, uint64_t param, uint64_t *h_dist_out,
                           sssp_run_stats *stats);
 
+/* Multi-source batch with read-back, the end-to-end call for many sources: runs
+ * h_sources[0..k) one after another and copies each result to HOST memory
+ * h_dist_out[i*n .. (i+1)*n) (pinned memory recommended).  The read-back of run i (a
+ * second stream, two internal distance buffers) overlaps run i+1, so the batch costs
+ * about max(kernel, copy) per source instead of their sum.  opts as for sssp_run_ex
+ * except SSSP_RUN_STATS (per run only).  stats (nullable): rounds summed over the batch,
+ * kernel_ms = the whole batch including read-backs.  Synchronous.  Errors as sssp_run,
+ * plus SSSP_ERR_INVALID for k < 0, NULL buffers or SSSP_RUN_STATS. */
+sssp_status sssp_run_batch_host(sssp_handle *h, const int32_t *h_sources, int32_t k, sssp_policy policy,
+                                uint64_t param, const sssp_run_opts *opts, uint64_t *h_dist_out,
+                                sssp_run_stats *stats);
+
 /* Releases host-side state only; never frees caller memory. */
 sssp_status sssp_destroy(sssp_handle *h);
 

@@ -75,6 +75,8 @@ _sigs = {
     "sssp_run_ex": (_st, [_vp, _i32, ctypes.c_int, _u64, ctypes.POINTER(sssp_run_opts), _vp,
                           ctypes.POINTER(sssp_run_stats)]),
     "sssp_run_host": (_st, [_vp, _i32, ctypes.c_int, _u64, _vp, ctypes.POINTER(sssp_run_stats)]),
+    "sssp_run_batch_host": (_st, [_vp, _vp, _i32, ctypes.c_int, _u64, ctypes.POINTER(sssp_run_opts), _vp,
+                                  ctypes.POINTER(sssp_run_stats)]),
     "sssp_destroy": (_st, [_vp]),
     "sssp_pq_workspace_bytes": (_sz, [_i32]),
     "sssp_pq_create": (_st, [_i32, _vp, _vp, _sz, _vp, ctypes.POINTER(_vp)]),
@@ -209,6 +211,25 @@ class SSSP:
         st = sssp_run_stats()
         _check(sssp_run_host(self._h, int(source), pol, int(param), ctypes.c_void_p(out_host.data_ptr()),
                              ctypes.byref(st)), "sssp_run_host")
+        self.last_stats = st.as_dict()
+        return out_host
+
+    def run_batch_host(self, sources, policy="rho", param=0, out_host=None, seed=0):
+        """End-to-end multi-source call: k sources, k x n distances in host memory (pinned
+        tensor recommended); the read-back of one source overlaps the next run."""
+        import numpy as np
+
+        torch = _torch()
+        pol = POLICIES[policy] if isinstance(policy, str) else int(policy)
+        src = np.ascontiguousarray(np.asarray(sources, dtype=np.int32))
+        k = len(src)
+        if out_host is None:
+            out_host = torch.empty((k, self.n), dtype=torch.int64, pin_memory=True)
+        o = sssp_run_opts()
+        o.seed = seed
+        st = sssp_run_stats()
+        _check(sssp_run_batch_host(self._h, ctypes.c_void_p(src.ctypes.data), k, pol, int(param), ctypes.byref(o),
+                                   ctypes.c_void_p(out_host.data_ptr()), ctypes.byref(st)), "sssp_run_batch_host")
         self.last_stats = st.as_dict()
         return out_host
 

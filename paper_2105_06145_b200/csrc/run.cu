@@ -33,18 +33,29 @@ struct sssp_handle {
     uint32_t flags;
     RunParams base;  // carved workspace pointers
     uint64_t* ws_dist;
+    uint64_t* ws_dist2;  // second internal distance buffer (batch runs double-buffer)
     Ctrl* ctrl;
     Ctrl* h_ctrl;  // pinned host mirror for result readback
     int device;
     cudaEvent_t ev[2];
     int num_sms;
     int grid[5][2][4];
+    // batch runs: a copy stream overlaps the read-back of run i with run i+1
+    cudaStream_t copy_stream;
+    cudaEvent_t ev_done[2], ev_copied[2];
+    struct RunStatus {
+        int32_t status;
+        int32_t pad;
+        int64_t rounds;
+    } * h_status;  // pinned, one per run of a batch
+    int32_t h_status_cap;
 };
 
 namespace {
 
 struct Layout {
     uint64_t* dist;
+    uint64_t* dist2;
     int32_t *q0, *q1;
     int64_t qcap;
     Desc* chunks;
@@ -79,6 +90,7 @@ Layout carve(void* base, int32_t n, int64_t m) {
     L.cta_delta = c.take<int64_t>((size_t)3 * kMaxCtas);
     L.cta_front = c.take<int64_t>((size_t)3 * kMaxCtas);
     L.dist = c.take<uint64_t>(n);
+    L.dist2 = c.take<uint64_t>(n);
     L.q0 = c.take<int32_t>(qlen);
     L.q1 = c.take<int32_t>(qlen);
     L.chunks = c.take<Desc>(clen);
@@ -99,6 +111,55 @@ KernelFn kernel_for(int pol, bool stats, int mode) {
         case SSSP_DELTA_STEPPING: return bidir ? kernel_table_4_1(stats, fuse) : kernel_table_4_0(stats, fuse);
     }
     return nullptr;
+}
+
+
+// Validate and enqueue one run of the round loop on h->stream (no synchronisation).
+sssp_status launch_run(sssp_handle* h, int32_t source, sssp_policy policy, uint64_t param, const sssp_run_opts& o,
+                       uint64_t* d_dist_out, int* grid_out, int64_t* max_rounds_out) {
+    if (!d_dist_out) return set_error(SSSP_ERR_INVALID, "sssp_run: NULL d_dist_out");
+    if (source < 0 || source >= h->n) return set_error(SSSP_ERR_RANGE, "sssp_run: source %d outside [0, %d)", source, h->n);
+    if (policy < SSSP_RHO || policy > SSSP_DELTA_STEPPING)
+        return set_error(SSSP_ERR_INVALID, "sssp_run: unknown policy %d", (int)policy);
+    if ((policy == SSSP_RHO || policy == SSSP_DELTA || policy == SSSP_DELTA_STEPPING) && param == 0)
+        return set_error(SSSP_ERR_INVALID, "sssp_run: param (rho / Delta) must be >= 1");
+    cudaError_t de = cudaSetDevice(h->device);
+    if (de != cudaSuccess) return cuda_error(de, "cudaSetDevice");
+    const bool st = (o.flags & SSSP_RUN_STATS) != 0;
+    // fusion ("local relaxation within theta", P:1381-1390) in live rounds of sparse graphs:
+    // the paper applies it when the average degree is below 20 (P:1385-1388)
+    // (measured: fusing the low-degree late rounds of R-MAT re-relaxes 17% more arcs and
+    // costs 50% time, so dense graphs do not fuse at all; see DESIGN.md fusion)
+    const bool fu = !(o.flags & (SSSP_RUN_SNAPSHOT | SSSP_RUN_NO_FUSE)) && policy != SSSP_DIJKSTRA &&
+                    h->m < (int64_t)kSparseDeg * h->n;
+    RunParams p = h->base;
+    p.dist = d_dist_out;
+    p.source = source;
+    p.param = param;
+    p.flags = o.flags;
+    p.seed = o.seed;
+    p.max_rounds = o.max_rounds > 0 ? o.max_rounds : 4 * (int64_t)h->n + 64;
+    p.trace = st ? (sssp_round*)o.d_trace : nullptr;
+    p.trace_cap = o.trace_cap;
+    p.ext_count = o.d_ext_count;
+    p.fuse_budget = o.fuse_budget ? (int32_t)o.fuse_budget : kFuseBudget;
+    const int mode = (fu ? 1 : 0) | ((o.flags & SSSP_RUN_BIDIR) ? 2 : 0);
+    KernelFn k = kernel_for(policy, st, mode);
+    const int grid = h->grid[policy][st][mode];
+    void* args[] = {&p};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kBlock), args, smem_bytes(fu), h->stream);
+    if (e != cudaSuccess) return cuda_error(e, "round-loop launch");
+    *grid_out = grid;
+    *max_rounds_out = p.max_rounds;
+    return SSSP_OK;
+}
+
+sssp_status run_status(int32_t status, int64_t max_rounds) {
+    if (status == SSSP_ERR_ROUNDS)
+        return set_error(SSSP_ERR_ROUNDS, "sssp_run: exceeded max_rounds=%lld", (long long)max_rounds);
+    if (status == SSSP_ERR_INTERNAL)
+        return set_error(SSSP_ERR_INTERNAL, "sssp_run: an append list overflowed its spill segment (bug)");
+    return SSSP_OK;
 }
 
 }  // namespace
@@ -146,6 +207,7 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
     h->device = dev;
     h->num_sms = sms;
     h->ws_dist = L.dist;
+    h->ws_dist2 = L.dist2;
     h->ctrl = L.ctrl;
     RunParams& b = h->base;
     memset(&b, 0, sizeof(b));
@@ -186,6 +248,11 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
     e = cudaMallocHost((void**)&h->h_ctrl, sizeof(Ctrl));
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev[0]);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev[1]);
+    for (int i = 0; i < 2 && e == cudaSuccess; i++) {
+        e = cudaEventCreateWithFlags(&h->ev_done[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_copied[i], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         delete h;
         return cuda_error(e, "sssp_create: host resources");
@@ -219,44 +286,17 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
 sssp_status sssp_run_ex(sssp_handle* h, int32_t source, sssp_policy policy, uint64_t param,
                         const sssp_run_opts* opts, uint64_t* d_dist_out, sssp_run_stats* stats) {
     if (!h) return set_error(SSSP_ERR_INVALID, "sssp_run: NULL handle");
-    if (!d_dist_out) return set_error(SSSP_ERR_INVALID, "sssp_run: NULL d_dist_out");
-    if (source < 0 || source >= h->n) return set_error(SSSP_ERR_RANGE, "sssp_run: source %d outside [0, %d)", source, h->n);
-    if (policy < SSSP_RHO || policy > SSSP_DELTA_STEPPING) return set_error(SSSP_ERR_INVALID, "sssp_run: unknown policy %d", (int)policy);
-    if ((policy == SSSP_RHO || policy == SSSP_DELTA || policy == SSSP_DELTA_STEPPING) && param == 0)
-        return set_error(SSSP_ERR_INVALID, "sssp_run: param (rho / Delta) must be >= 1");
-    cudaError_t de = cudaSetDevice(h->device);
-    if (de != cudaSuccess) return cuda_error(de, "cudaSetDevice");
     sssp_run_opts o;
     memset(&o, 0, sizeof(o));
     if (opts) o = *opts;
-    const bool st = (o.flags & SSSP_RUN_STATS) != 0;
-    // fusion ("local relaxation within theta", P:1381-1390) in live rounds of sparse graphs:
-    // the paper applies it when the average degree is below 20 (P:1385-1388)
-    // (measured: fusing the low-degree late rounds of R-MAT re-relaxes 17% more arcs and
-    // costs 50% time, so dense graphs do not fuse at all; see DESIGN.md fusion)
-    const bool fu = !(o.flags & (SSSP_RUN_SNAPSHOT | SSSP_RUN_NO_FUSE)) && policy != SSSP_DIJKSTRA &&
-                    h->m < (int64_t)kSparseDeg * h->n;
-    RunParams p = h->base;
-    p.dist = d_dist_out;
-    p.source = source;
-    p.param = param;
-    p.flags = o.flags;
-    p.seed = o.seed;
-    p.max_rounds = o.max_rounds > 0 ? o.max_rounds : 4 * (int64_t)h->n + 64;
-    p.trace = st ? (sssp_round*)o.d_trace : nullptr;
-    p.trace_cap = o.trace_cap;
-    p.ext_count = o.d_ext_count;
-    p.fuse_budget = o.fuse_budget ? (int32_t)o.fuse_budget : kFuseBudget;
-    const int mode = (fu ? 1 : 0) | ((o.flags & SSSP_RUN_BIDIR) ? 2 : 0);
-    KernelFn k = kernel_for(policy, st, mode);
-    const int grid = h->grid[policy][st][mode];
-    void* args[] = {&p};
+    int grid = 0;
+    int64_t max_rounds = 0;
     cudaEventRecord(h->ev[0], h->stream);
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kBlock), args, smem_bytes(fu), h->stream);
-    if (e != cudaSuccess) return cuda_error(e, "round-loop launch");
+    sssp_status st = launch_run(h, source, policy, param, o, d_dist_out, &grid, &max_rounds);
+    if (st != SSSP_OK) return st;
     cudaEventRecord(h->ev[1], h->stream);
-    e = cudaMemcpyAsync(&h->h_ctrl->status, &h->ctrl->status, sizeof(Ctrl) - offsetof(Ctrl, status),
-                        cudaMemcpyDeviceToHost, h->stream);
+    cudaError_t e = cudaMemcpyAsync(&h->h_ctrl->status, &h->ctrl->status, sizeof(Ctrl) - offsetof(Ctrl, status),
+                                    cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) return cuda_error(e, "round loop");
     const Ctrl* c = h->h_ctrl;
@@ -277,10 +317,70 @@ sssp_status sssp_run_ex(sssp_handle* h, int32_t source, sssp_policy policy, uint
         cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]);
         stats->kernel_ms = ms;
     }
-    if (c->status == SSSP_ERR_ROUNDS)
-        return set_error(SSSP_ERR_ROUNDS, "sssp_run: exceeded max_rounds=%lld", (long long)p.max_rounds);
-    if (c->status == SSSP_ERR_INTERNAL)
-        return set_error(SSSP_ERR_INTERNAL, "sssp_run: an append list overflowed its spill segment (bug)");
+    return run_status(c->status, max_rounds);
+}
+
+sssp_status sssp_run_batch_host(sssp_handle* h, const int32_t* h_sources, int32_t k, sssp_policy policy,
+                                uint64_t param, const sssp_run_opts* opts, uint64_t* h_dist_out,
+                                sssp_run_stats* stats) {
+    if (!h) return set_error(SSSP_ERR_INVALID, "sssp_run_batch_host: NULL handle");
+    if (k < 0 || (k > 0 && (!h_sources || !h_dist_out)))
+        return set_error(SSSP_ERR_INVALID, "sssp_run_batch_host: bad batch (k=%d)", k);
+    sssp_run_opts o;
+    memset(&o, 0, sizeof(o));
+    if (opts) o = *opts;
+    if (o.flags & SSSP_RUN_STATS)
+        return set_error(SSSP_ERR_INVALID, "sssp_run_batch_host: SSSP_RUN_STATS is per run (use sssp_run_ex)");
+    cudaError_t e = cudaSetDevice(h->device);
+    if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
+    if (k > h->h_status_cap) {
+        if (h->h_status) cudaFreeHost(h->h_status);
+        h->h_status = nullptr;
+        h->h_status_cap = 0;
+        e = cudaMallocHost((void**)&h->h_status, (size_t)k * sizeof(sssp_handle::RunStatus));
+        if (e != cudaSuccess) return cuda_error(e, "sssp_run_batch_host: pinned status buffer");
+        h->h_status_cap = k;
+    }
+    uint64_t* buf[2] = {h->ws_dist, h->ws_dist2};
+    const size_t bytes = (size_t)h->n * sizeof(uint64_t);
+    int grid = 0;
+    int64_t max_rounds = 0;
+    cudaEventRecord(h->ev[0], h->stream);
+    for (int32_t i = 0; i < k; i++) {
+        const int b = i & 1;
+        if (i >= 2) cudaStreamWaitEvent(h->stream, h->ev_copied[b], 0);  // buffer b read back
+        sssp_status st = launch_run(h, h_sources[i], policy, param, o, buf[b], &grid, &max_rounds);
+        if (st != SSSP_OK) {
+            cudaStreamSynchronize(h->stream);
+            cudaStreamSynchronize(h->copy_stream);
+            return st;
+        }
+        cudaMemcpyAsync(&h->h_status[i], &h->ctrl->status, sizeof(sssp_handle::RunStatus), cudaMemcpyDeviceToHost,
+                        h->stream);
+        cudaEventRecord(h->ev_done[b], h->stream);
+        cudaStreamWaitEvent(h->copy_stream, h->ev_done[b], 0);
+        cudaMemcpyAsync(h_dist_out + (size_t)i * h->n, buf[b], bytes, cudaMemcpyDeviceToHost, h->copy_stream);
+        cudaEventRecord(h->ev_copied[b], h->copy_stream);
+    }
+    cudaEventRecord(h->ev[1], h->copy_stream);
+    e = cudaStreamSynchronize(h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->copy_stream);
+    if (e != cudaSuccess) return cuda_error(e, "sssp_run_batch_host");
+    int64_t rounds = 0;
+    for (int32_t i = 0; i < k; i++) {
+        rounds += h->h_status[i].rounds;
+        sssp_status st = run_status(h->h_status[i].status, max_rounds);
+        if (st != SSSP_OK) return st;
+    }
+    if (stats) {
+        memset(stats, 0, sizeof(*stats));
+        stats->rounds = rounds;
+        stats->grid_blocks = grid;
+        stats->block_threads = kBlock;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]);
+        stats->kernel_ms = ms;  // whole batch, read-backs included
+    }
     return SSSP_OK;
 }
 
@@ -307,6 +407,12 @@ sssp_status sssp_destroy(sssp_handle* h) {
     if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
     if (h->ev[0]) cudaEventDestroy(h->ev[0]);
     if (h->ev[1]) cudaEventDestroy(h->ev[1]);
+    for (int i = 0; i < 2; i++) {
+        if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
+        if (h->ev_copied[i]) cudaEventDestroy(h->ev_copied[i]);
+    }
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    if (h->h_status) cudaFreeHost(h->h_status);
     delete h;
     return SSSP_OK;
 }

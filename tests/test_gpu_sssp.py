@@ -276,3 +276,20 @@ def test_bidirectional_undirected(cuda_device):
                          ("dijkstra", 0)):
             for kw in (dict(), dict(snapshot=True), dict(fuse=False)):
                 _assert_same(_run(h, g, pol, par, bidir=True, **kw), want, f"{g.name}/{pol}/{par}/{kw}/bidir")
+
+
+def test_batch_host(cuda_device):
+    """sssp_run_batch_host: k sources, each result read back to host while the next runs."""
+    P = _P()
+    for name in ("rmat14log", "grid64"):
+        g = gen.make(name)
+        h = P.SSSP.from_graph(g)
+        rs = np.random.default_rng(9)
+        sources = [g.source] + [int(x) for x in rs.integers(0, g.n, 6)]
+        for pol, par in (("rho", 256), ("delta", 5000), ("bellman_ford", 0)):
+            out = h.run_batch_host(sources, pol, par).numpy().view(np.uint64)
+            for i, s in enumerate(sources):
+                _assert_same(out[i], oracle.dijkstra(g, s), f"{name}/{pol}/batch{i}")
+        assert h.run_batch_host([], "rho", 4).shape[0] == 0
+        with pytest.raises(P.SSSPError):
+            h.run_batch_host([0, g.n], "rho", 4)
