@@ -76,14 +76,18 @@ typedef struct sssp_handle sssp_handle;
 #define SSSP_VALIDATE 1u /* check the CSR on the device at create time (one extra kernel) */
 
 /* Bytes of device workspace a handle for an n-vertex, m-arc graph needs (flags as
- * for sssp_create).  Holds the LaB-PQ (bitmap, two queues), the extracted
- * frontier, the heavy-vertex chunk map, theta samples, an internal distance
- * array and the control block.  Returns 0 if n or m is out of range. */
+ * for sssp_create).  Holds an interleaved copy of the arcs ({head, weight}, 8m
+ * bytes), the LaB-PQ (two queues; the in-Q flag is bit 63 of each distance
+ * word), the heavy-vertex chunk map, theta samples, an internal distance array
+ * and the control block.  Returns 0 if n or m is out of range. */
 size_t sssp_workspace_bytes(int32_t n, int64_t m, uint32_t flags);
 
 /* Create a handle over a device-resident CSR.
  *   n in [1, 2^31-2], m in [0, 2^31-1]; d_offsets[n+1], d_indices[m], d_weights[m]
- *   are BORROWED device arrays (never freed by the library).  d_workspace is a
+ *   are BORROWED device arrays (never freed by the library).  d_offsets is read by
+ *   every run; d_indices / d_weights only by the copy into the workspace that
+ *   sssp_create enqueues on `stream` (they may be reused once that work is done,
+ *   a later change to them is not seen by the handle).  d_workspace is a
  *   borrowed device buffer of ws_bytes >= sssp_workspace_bytes(n, m, flags),
  *   256-byte aligned.  stream orders all later work.
  * Errors: SSSP_ERR_INVALID (null/size/alignment), SSSP_ERR_INVALID_GRAPH (with
@@ -136,6 +140,12 @@ typedef struct {
     int64_t dense;        /* vertices read by near/far dense passes this round           */
     int64_t busy_a_ns;    /* sum over warps of time spent in phase A before its barrier  */
     int64_t busy_b_ns;    /* sum over warps of time spent in phase B before its barrier  */
+    int64_t busy_a_max_ns; /* the slowest warp's phase-A time (busy_a_ns / warps = mean)  */
+    int64_t fused;        /* vertices extracted by fusion this round (included in fsize) */
+    int64_t t_near_ns;    /* part of t_theta_ns spent on near/far pulls and shrinks      */
+    int64_t prof_cyc[4];  /* -DSSSP_PROF=1 builds only (else 0): phase-A SM cycles summed over
+                             warps in scan / take (delete + CSR row) / light relax / queue
+                             flush (the flush also counts inside the relax part)           */
 } sssp_round;
 
 typedef struct {

@@ -10,6 +10,7 @@ import glob
 import os
 import subprocess
 import sys
+import tempfile
 from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -51,7 +52,9 @@ def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=())
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
     tag = os.path.splitext(os.path.basename(out))[0]
-    objdir = os.path.join(HERE, "build", tag)
+    # object files live outside the tree (they are ~40 MB per variant; only the linked
+    # .so travels with the repo snapshot)
+    objdir = os.path.join(os.environ.get("SSSP_BUILD_DIR", os.path.join(tempfile.gettempdir(), "sssp_build")), tag)
     os.makedirs(objdir, exist_ok=True)
     dflags = [f"-D{d}" for d in defines]
 

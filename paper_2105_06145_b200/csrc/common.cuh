@@ -30,6 +30,23 @@ __device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p) {
     asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
+// CSR row bounds off[i], off[i+1] in one 8-byte-or-two load pair, issued in program order
+// (asm volatile) so that it stays ahead of a following atom_or_u64 instead of being sunk
+// below the branch on the atomic's result
+__device__ __forceinline__ void ld_row(const int32_t* off, int32_t i, int32_t& beg, int32_t& end) {
+    asm volatile("ld.global.nc.s32 %0, [%2];\n\tld.global.nc.s32 %1, [%2+4];" : "=r"(beg), "=r"(end) : "l"(off + i));
+}
+__device__ __forceinline__ uint64_t atom_or_u64(uint64_t* p, uint64_t x) {
+    uint64_t old;
+    asm volatile("atom.global.or.b64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(x) : "memory");
+    return old;
+}
+// one interleaved arc {head, weight}: a single 8-byte load (one row, one TLB lookup)
+__device__ __forceinline__ uint2 ld_stream_arc(const uint2* p) {
+    uint2 a;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(a.x), "=r"(a.y) : "l"(p));
+    return a;
+}
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));

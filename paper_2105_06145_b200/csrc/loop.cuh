@@ -54,7 +54,7 @@ namespace sssp {
 #define SSSP_ARCS 4
 #endif
 #ifndef SSSP_LIGHT
-#define SSSP_LIGHT 128
+#define SSSP_LIGHT 32
 #endif
 constexpr uint64_t kTop = 1ull << 63;        // flag bit: set = not in Q
 constexpr uint64_t kVal = kTop - 1;          // value bits of a delta word
@@ -66,8 +66,11 @@ constexpr int kLight = SSSP_LIGHT;           // out-degree <= kLight: relaxed by
 constexpr int kSmemSamples = 2048;           // theta samples held in shared memory (else CTA-0 fallback)
 constexpr int kRankSelect = 256;             // s <= this: select by rank counting
 constexpr int kWarps = kBlock / 32;
+#ifndef SSSP_PROF
+#define SSSP_PROF 0  // 1: STATS kernels also split phase-A warp time into parts (clock64)
+#endif
 #ifndef SSSP_NEAR_K
-#define SSSP_NEAR_K 4
+#define SSSP_NEAR_K 8
 #endif
 #ifndef SSSP_L1DIST
 #define SSSP_L1DIST 1
@@ -118,7 +121,10 @@ struct __align__(128) RoundCnt {
     unsigned long long split;    // CTA-0 broadcast of a new near/far split
     unsigned long long busy_a;   // STATS: sum over warps of phase-A busy time (ns)
     unsigned long long busy_b;   // STATS: same for phase B
-    unsigned long long pad[7];
+    unsigned long long busy_a_max;  // STATS: slowest warp's phase-A busy time (ns)
+    unsigned long long fused;    // STATS: vertices extracted by fusion
+    unsigned long long prof[4];  // SSSP_PROF: phase-A cycles summed over warps: scan, take, relax, flush
+    unsigned long long pad[1];
 };
 
 struct __align__(128) Ctrl {
@@ -151,8 +157,7 @@ struct RunParams {
     int32_t source;
     int64_t m;
     const int32_t* __restrict__ off;
-    const int32_t* __restrict__ idx;
-    const uint32_t* __restrict__ w;
+    const uint2* __restrict__ arc;  // interleaved CSR arcs {head, weight} (workspace copy)
     uint64_t* dist;
     int32_t* qbuf[2];   // queue storage, ping-pong
     int64_t qcap;       // per-shard queue capacity
@@ -199,6 +204,9 @@ __device__ __forceinline__ void reset_cnt(RoundCnt* c) {
     c->split = 0;
     c->busy_a = 0;
     c->busy_b = 0;
+    c->busy_a_max = 0;
+    c->fused = 0;
+    for (int i = 0; i < 4; i++) c->prof[i] = 0;
 }
 
 __device__ __forceinline__ Desc ld_desc(const Desc* p) {
@@ -313,7 +321,19 @@ struct Warp {  // per-warp working state (qn is warp-uniform)
     int32_t fn;       // staged fused vertices (warp-uniform)
     int32_t fbudget;  // fusions left this round (warp-uniform)
     Acc acc;
+#if SSSP_PROF
+    uint64_t prof[4];  // cycles: scan, take, relax, flush (STATS kernels)
+#endif
 };
+
+// SSSP_PROF: add the cycles since t0 to part i of the warp's phase-A profile
+#if SSSP_PROF
+#define PROF_T0(t) const long long t = clock64()
+#define PROF_ADD(W, i, t) ((W).prof[i] += (uint64_t)(clock64() - (t)))
+#else
+#define PROF_T0(t)
+#define PROF_ADD(W, i, t)
+#endif
 
 // A successful WriteMin replaced word w_old by value c (flag cleared).  Returns true iff
 // v must be appended to the near queue: it was outside Q (insertion) and c <= split, or
@@ -354,6 +374,7 @@ __device__ __forceinline__ void reserve(const Sharded<T>& L, int shard, int32_t 
 
 __device__ __forceinline__ void wq_flush(Warp& W) {
     if (W.qn == 0) return;
+    PROF_T0(tf);
     __syncwarp();
     int32_t *p0, *p1;
     int32_t fit, lim;
@@ -367,6 +388,7 @@ __device__ __forceinline__ void wq_flush(Warp& W) {
     }
     __syncwarp();
     W.qn = 0;
+    PROF_ADD(W, 3, tf);
 }
 
 // stage the lanes' ids with pred (one id per lane)
@@ -489,8 +511,9 @@ __device__ __forceinline__ void relax_chunk(const RunParams& p, uint64_t d, int3
 #pragma unroll
     for (int t = 0; t < kArcs; t++) {
         const int32_t k = t * 32 + lane;
-        v[t] = k < len ? ld_stream_i32(p.idx + beg + k) : -1;
-        c[t] = d + (k < len ? ld_stream_u32(p.w + beg + k) : 0u);
+        const uint2 a = k < len ? ld_stream_arc(p.arc + beg + k) : make_uint2(0xFFFFFFFFu, 0u);
+        v[t] = (int32_t)a.x;
+        c[t] = d + a.y;
     }
     relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W);
 }
@@ -569,8 +592,9 @@ __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, i
             const int32_t rb = __shfl_sync(kFull, rowbase, o[t]);
             const uint64_t od = __shfl_sync(kFull, d, o[t]);
             const bool ok = e < total;
-            v[t] = ok ? ld_stream_i32(p.idx + rb + e) : -1;
-            wt[t] = ok ? ld_stream_u32(p.w + rb + e) : 0u;
+            const uint2 a = ok ? ld_stream_arc(p.arc + rb + e) : make_uint2(0xFFFFFFFFu, 0u);
+            v[t] = (int32_t)a.x;
+            wt[t] = a.y;
             c[t] = od + wt[t];
         }
         if (BIDIR && bidir)
@@ -671,20 +695,25 @@ template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __device__ __forceinline__ void take_batch(const RunParams& p, int32_t cnt, const Sharded<Desc>& CL, bool snap, Warp& W,
                                            uint64_t& fs, uint64_t& edges) {
     const int lane = lane_id();
+    PROF_T0(tt);
     __syncwarp();
     int32_t id = lane < cnt ? W.st->take[lane] : -1;
-    uint64_t d = 0;
-    int32_t beg = 0, deg = 0;
+    // the CSR row is read alongside the delete (independent loads: one latency, not two);
+    // the results are consumed by selects, not inside the branch, so they stay ahead of it
+    int32_t beg = 0, end = 0;
+    uint64_t old = kTop;
     if (id >= 0) {
-        const uint64_t old = atomicOr((unsigned long long*)(p.dist + id), (unsigned long long)kTop);  // delete from Q
-        d = old & kVal;
-        if (old & kTop) id = -1;  // already deleted by another copy (safety net: copies are not expected)
+        ld_row(p.off, id, beg, end);
+        old = atom_or_u64(p.dist + id, kTop);  // delete from Q
     }
+    const bool ok = !(old & kTop);  // else already deleted by another copy (safety net: not expected)
+    const uint64_t d = old & kVal;
+    const int32_t deg = ok ? end - beg : 0;
+    beg = ok ? beg : 0;
+    id = ok ? id : -1;
     if (id >= 0) {
         W.qdelta--;
         W.front += 1;
-        beg = __ldg(p.off + id);
-        deg = __ldg(p.off + id + 1) - beg;
         W.front += (uint64_t)deg << 32;
         if (p.ext_count) atomicAdd(p.ext_count + id, 1);
     }
@@ -699,8 +728,13 @@ __device__ __forceinline__ void take_batch(const RunParams& p, int32_t cnt, cons
         const int32_t ls = warp_append_slot(light, &W.C->nlight);
         if (light) st_desc(p.light + ls, d, beg, deg);
     } else if (__any_sync(kFull, light)) {
+        PROF_ADD(W, 1, tt);
+        PROF_T0(tr);
         relax_vertices<POL, STATS, FUSE, BIDIR>(p, d, beg, light ? deg : 0, W, light ? id : -1);
+        PROF_ADD(W, 2, tr);
+        return;
     }
+    PROF_ADD(W, 1, tt);
 }
 
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
@@ -724,6 +758,7 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
     const int64_t hi = contig ? (gw + 1) * q / nwarps : q;
     const int64_t stride = contig ? 32 * ent : nwarps * (32 * ent);
     for (int64_t base = lo; base < hi; base += stride) {
+        PROF_T0(ts);
         int32_t id[kEnt];
         uint64_t val[kEnt];
         const int sg = seg_of(qpref, base);  // warp-uniform
@@ -749,6 +784,7 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
             if (take) W.st->take[tn + __popc(tm & lanemask_lt())] = id[e];
             tn += __popc(tm);
         }
+        PROF_ADD(W, 0, ts);
         int32_t done = 0;
         while (tn - done >= 32) {
             if (done) {  // move the next 32 to the front (take_batch reads take[0..32))
@@ -837,6 +873,7 @@ __device__ __forceinline__ void flush_acc(const RunParams& p, int64_t r, Warp& W
         if (lane_id() == 0 && s) atomicAdd(&W.C->succ, (unsigned long long)s);
         if (lane_id() == 0 && ins) atomicAdd(&W.C->inserts, (unsigned long long)ins);
         if (lane_id() == 0 && fu) atomicAdd(&W.C->fsize, (unsigned long long)fu);
+        if (lane_id() == 0 && fu) atomicAdd(&W.C->fused, (unsigned long long)fu);
         if (lane_id() == 0 && fe) atomicAdd(&W.C->edges, (unsigned long long)fe);
     }
     W.acc.succ = 0;
@@ -972,6 +1009,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     W.fn = 0;
     W.qdelta = 0;
     W.front = 0;
+#if SSSP_PROF
+    for (int i = 0; i < 4; i++) W.prof[i] = 0;
+#endif
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
 
@@ -1037,9 +1077,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             if (gtid == 0) ctrl->status = SSSP_ERR_ROUNDS;
             break;
         }
-        uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+        uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0, tn = 0;
         int64_t dense = 0;
-        if (STATS && gtid == 0) t0 = globaltimer();
+        if (STATS && gtid == 0) t0 = tn = globaltimer();
         if (gtid == 0) reset_cnt(&ctrl->cnt[(r + 1) % 3]);
         if (gtid < 2 * kSeg) {  // counters of slot (r+1)%3: written in round r+1, read in r+1 / r+2
             p.counters[((int64_t)(((r + 1) % 3) * 2) * kSeg + gtid) * kCntStride] = 0;
@@ -1140,6 +1180,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                     snap = true;
                 }
             }
+            if (STATS && gtid == 0) tn = globaltimer();
             const uint64_t s = sample_count((uint64_t)qn, rho);
             if ((uint64_t)qtot <= rho) {
                 theta = kInf;  // |Q| <= rho: extract all
@@ -1189,7 +1230,17 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         uint64_t minrem = kInf;
         const uint64_t ta = STATS ? globaltimer() : 0;
         phase_a<POL, STATS, FUSE, BIDIR>(p, QC, qpref, CL, theta, snap, minrem, W);
-        if (STATS && lane_id() == 0) atomicAdd(&C->busy_a, (unsigned long long)(globaltimer() - ta));
+        if (STATS && lane_id() == 0) {
+            const unsigned long long ba = globaltimer() - ta;
+            atomicAdd(&C->busy_a, ba);
+            atomicMax(&C->busy_a_max, ba);
+#if SSSP_PROF
+            for (int i = 0; i < 4; i++) atomicAdd(&C->prof[i], (unsigned long long)W.prof[i]);
+#endif
+        }
+#if SSSP_PROF
+        for (int i = 0; i < 4; i++) W.prof[i] = 0;
+#endif
         flush_acc<POL, STATS, FUSE, BIDIR>(p, r, W);
         grid_sync(nullptr);
         if (STATS && gtid == 0) t2 = globaltimer();
@@ -1240,6 +1291,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                 t->dense = dense;
                 t->busy_a_ns = (int64_t)C->busy_a;
                 t->busy_b_ns = (int64_t)C->busy_b;
+                t->busy_a_max_ns = (int64_t)C->busy_a_max;
+                t->fused = (int64_t)C->fused;
+                t->t_near_ns = (int64_t)(tn - t0);
+                for (int i = 0; i < 4; i++) t->prof_cyc[i] = (int64_t)C->prof[i];
             }
             ctrl->tot_extracted += f;
             ctrl->tot_edges += (int64_t)C->edges;

@@ -4,6 +4,17 @@
 
 namespace sssp {
 
+// --------------------------------------------------------------------- arc interleave
+// arc[e] = {idx[e], w[e]}: the relax reads an arc's head and weight with one 8-byte load,
+// so a light vertex's row costs one TLB lookup in one 8m-byte array instead of one in
+// each of two 4m-byte arrays (random rows over GBs are TLB-miss bound)
+__global__ void interleave_arcs(int64_t m, const int32_t* __restrict__ idx, const uint32_t* __restrict__ w,
+                                uint2* __restrict__ arc) {
+    const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gsize)
+        arc[e] = make_uint2((uint32_t)idx[e], w[e]);
+}
+
 // --------------------------------------------------------------------- CSR validation
 __global__ void validate_csr(int32_t n, int64_t m, const int32_t* off, const int32_t* idx, const uint32_t* w,
                              int32_t* err) {
@@ -54,6 +65,7 @@ struct sssp_handle {
 namespace {
 
 struct Layout {
+    uint2* arc;  // interleaved {head, weight} copy of the CSR arcs
     uint64_t* dist;
     uint64_t* dist2;
     int32_t *q0, *q1;
@@ -83,6 +95,7 @@ Layout carve(void* base, int32_t n, int64_t m) {
     L.ccap = 2 * ((ctot + kShards - 1) / kShards) + 256;
     L.cspill = ctot;
     const int64_t clen = kShards * L.ccap + ctot;
+    L.arc = c.take<uint2>((size_t)m);
     L.ctrl = c.take<Ctrl>(1);
     L.err = c.take<int32_t>(32);
     L.counters = c.take<int32_t>((size_t)3 * 2 * kSeg * kCntStride);
@@ -214,8 +227,7 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
     b.n = n;
     b.m = m;
     b.off = d_offsets;
-    b.idx = d_indices;
-    b.w = d_weights;
+    b.arc = L.arc;
     b.qbuf[0] = L.q0;
     b.qbuf[1] = L.q1;
     b.qcap = L.qcap;
@@ -273,6 +285,10 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
                              (herr & 1) ? "offsets[0]!=0 or offsets[n]!=m " : "", (herr & 2) ? "offsets decrease " : "",
                              (herr & 4) ? "index out of range " : "", (herr & 8) ? "weight < 1" : "");
         }
+    }
+    if (e == cudaSuccess && m > 0) {
+        interleave_arcs<<<sms * 8, 256, 0, h->stream>>>(m, d_indices, d_weights, L.arc);
+        e = cudaGetLastError();
     }
     if (e != cudaSuccess) {
         cudaFreeHost(h->h_ctrl);

@@ -55,10 +55,10 @@ def test_workspace_sizing_host_only():
     assert small > 0
     n, m = 1 << 24, 520_000_000
     big = P.sssp_workspace_bytes(n, m, 0)
-    # dist x2 16n + two sharded queues (3n ids each) 24n + light frontier 16n = 56n; chunk
-    # descriptors: 3 x 16 B x (m/chunk + m/(light+1)) with chunk >= 128 arcs and light >= 64
-    # (sharded at 2x + spill); counters/samples < 64 MiB
-    assert 56 * n < big < 56 * n + 48 * (m // 128 + m // 65 + 1) + (64 << 20)
+    # interleaved arcs 8m; dist x2 16n + two sharded queues (3n ids each) 24n + light
+    # frontier 16n = 56n; chunk descriptors: 3 x 16 B x (m/chunk + m/(light+1)) with
+    # chunk >= 128 arcs and light >= 32 (sharded at 2x + spill); counters/samples < 64 MiB
+    assert 8 * m + 56 * n < big < 8 * m + 56 * n + 48 * (m // 128 + m // 33 + 1) + (64 << 20)
     assert P.sssp_pq_workspace_bytes(1000) > 8 * 1000 // 8
 
 
