@@ -143,9 +143,11 @@ typedef struct {
     int64_t busy_a_max_ns; /* the slowest warp's phase-A time (busy_a_ns / warps = mean)  */
     int64_t fused;        /* vertices extracted by fusion this round (included in fsize) */
     int64_t t_near_ns;    /* part of t_theta_ns spent on near/far pulls and shrinks      */
-    int64_t prof_cyc[4];  /* -DSSSP_PROF=1 builds only (else 0): phase-A SM cycles summed over
-                             warps in scan / take (delete + CSR row) / light relax / queue
-                             flush (the flush also counts inside the relax part)           */
+    int64_t prof[8];      /* -DSSSP_PROF=1 builds only (else 0), phase A summed over warps:
+                             SM cycles in scan / take (delete + CSR row) / light relax /
+                             queue flush / fuse_drain, fuse_drain batches, relax steps,
+                             SM cycles in relax steps (parts overlap: flush and relax
+                             steps also count inside the relax and fuse parts)            */
 } sssp_round;
 
 typedef struct {

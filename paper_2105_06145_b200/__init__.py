@@ -63,7 +63,8 @@ class sssp_run_stats(ctypes.Structure):
 
 ROUND_FIELDS = ["qsize", "fsize", "edges", "inserts", "succ", "theta", "nheavy", "t_theta_ns", "t_extract_ns",
                 "t_relax_ns", "qnear", "dense", "busy_a_ns", "busy_b_ns",
-                "busy_a_max_ns", "fused", "t_near_ns", "prof_scan", "prof_take", "prof_relax", "prof_flush"]
+                "busy_a_max_ns", "fused", "t_near_ns", "prof_scan", "prof_take", "prof_relax", "prof_flush",
+                "prof_fuse", "prof_fuse_batches", "prof_steps", "prof_step_cyc"]
 ROUND_WORDS = len(ROUND_FIELDS)
 
 _vp, _i32, _i64, _u64, _u32, _sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,

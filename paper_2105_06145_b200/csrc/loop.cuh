@@ -97,6 +97,7 @@ constexpr int kSeg = kShards + 1;
 constexpr int kCntStride = 256;              // int32 words between counters (1 KB: distinct L2 slices)
 constexpr int kMaxCtas = 4096;
 constexpr int kPolicies = 5;
+constexpr int kProf = 8;                     // SSSP_PROF counters per round
 constexpr int kNearK = SSSP_NEAR_K;          // near queue target: ~kNearK rounds of extraction
 constexpr int kFarSamples = 1024;            // vertices probed to place a new near/far split
 static_assert(32 * kArcs <= kQBuf, "one relax step must fit the stage");
@@ -123,8 +124,7 @@ struct __align__(128) RoundCnt {
     unsigned long long busy_b;   // STATS: same for phase B
     unsigned long long busy_a_max;  // STATS: slowest warp's phase-A busy time (ns)
     unsigned long long fused;    // STATS: vertices extracted by fusion
-    unsigned long long prof[4];  // SSSP_PROF: phase-A cycles summed over warps: scan, take, relax, flush
-    unsigned long long pad[1];
+    unsigned long long prof[kProf];  // SSSP_PROF: phase-A warp sums (see Warp::prof)
 };
 
 struct __align__(128) Ctrl {
@@ -206,7 +206,7 @@ __device__ __forceinline__ void reset_cnt(RoundCnt* c) {
     c->busy_b = 0;
     c->busy_a_max = 0;
     c->fused = 0;
-    for (int i = 0; i < 4; i++) c->prof[i] = 0;
+    for (int i = 0; i < kProf; i++) c->prof[i] = 0;
 }
 
 __device__ __forceinline__ Desc ld_desc(const Desc* p) {
@@ -322,7 +322,9 @@ struct Warp {  // per-warp working state (qn is warp-uniform)
     int32_t fbudget;  // fusions left this round (warp-uniform)
     Acc acc;
 #if SSSP_PROF
-    uint64_t prof[4];  // cycles: scan, take, relax, flush (STATS kernels)
+    // cycles in scan, take, light relax, queue flush, fuse_drain; fuse_drain batches;
+    // relax steps (relax_slots calls); cycles in relax_slots
+    uint64_t prof[kProf];
 #endif
 };
 
@@ -439,12 +441,16 @@ struct NoPull {
 template <int POL, bool STATS, bool FUSE, bool BIDIR, typename Pull = NoPull>
 __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&v)[kArcs], uint64_t (&c)[kArcs],
                                             Warp& W, Pull pull = Pull()) {
+    PROF_T0(trs);
+#if SSSP_PROF
+    W.prof[6]++;
+#endif
+    // room for a full step of fusions and budget left (warp-uniform)
+    const bool fuse = FUSE && W.fuse_theta != 0 && W.fbudget > 0 && W.fn <= kFBuf - 32 * kArcs;
     uint64_t cur[kArcs];
 #pragma unroll
     for (int t = 0; t < kArcs; t++) cur[t] = v[t] >= 0 ? dist_filter_ld(p.dist + v[t]) : 0ull;
     pull(v, cur, c);  // bidirectional relaxation may lower the candidates (SURVEY f-2)
-    // room for a full step of fusions and budget left (warp-uniform)
-    const bool fuse = FUSE && W.fuse_theta != 0 && W.fbudget > 0 && W.fn <= kFBuf - 32 * kArcs;
     // first CAS attempt of every slot issued back to back (one round trip, not kArcs),
     // then the rare retries
     uint64_t old[kArcs];
@@ -499,6 +505,7 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
         W.fn += tot;
         W.fbudget -= tot;
     }
+    PROF_ADD(W, 7, trs);
 }
 
 // One chunk: arcs [beg, beg+len) of a vertex with key d, len <= kChunk.  Lane-strided
@@ -605,12 +612,18 @@ __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, i
 }
 
 // Relax the fused vertices (already deleted from / never entered Q, key known), 32 at a
-// time from the top of the warp's stack; their relaxations may fuse more.
+// time from the top of the warp's stack; their relaxations may fuse more.  (The order
+// matters: tried together with a lane-local relax for degree <= kArcs, a FIFO ring and
+// slot-major pushes scanned 6-7x more arcs on grid4096 with Delta* = 2^17, 40-55 % slower.)
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __device__ __forceinline__ void fuse_drain(const RunParams& p, Warp& W) {
     if (!FUSE) return;
     const int lane = lane_id();
+    PROF_T0(tfd);
     while (W.fn > 0) {
+#if SSSP_PROF
+        W.prof[5]++;
+#endif
         const int32_t cnt = W.fn < 32 ? W.fn : 32;
         __syncwarp();
         int32_t id = -1;
@@ -648,6 +661,7 @@ __device__ __forceinline__ void fuse_drain(const RunParams& p, Warp& W) {
         }
         relax_vertices<POL, STATS, FUSE, BIDIR>(p, d, beg, deg, W, id);
     }
+    PROF_ADD(W, 4, tfd);
 }
 
 // Cut the heavy lanes' vertices into kChunk-arc descriptors (one reservation per warp).
@@ -1010,7 +1024,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     W.qdelta = 0;
     W.front = 0;
 #if SSSP_PROF
-    for (int i = 0; i < 4; i++) W.prof[i] = 0;
+    for (int i = 0; i < kProf; i++) W.prof[i] = 0;
 #endif
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
@@ -1229,17 +1243,20 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         // ---- phase A: Extract(theta) (+ light relax in live mode)
         uint64_t minrem = kInf;
         const uint64_t ta = STATS ? globaltimer() : 0;
+#if SSSP_PROF
+        for (int i = 0; i < kProf; i++) W.prof[i] = 0;  // phase-A only
+#endif
         phase_a<POL, STATS, FUSE, BIDIR>(p, QC, qpref, CL, theta, snap, minrem, W);
         if (STATS && lane_id() == 0) {
             const unsigned long long ba = globaltimer() - ta;
             atomicAdd(&C->busy_a, ba);
             atomicMax(&C->busy_a_max, ba);
 #if SSSP_PROF
-            for (int i = 0; i < 4; i++) atomicAdd(&C->prof[i], (unsigned long long)W.prof[i]);
+            for (int i = 0; i < kProf; i++) atomicAdd(&C->prof[i], (unsigned long long)W.prof[i]);
 #endif
         }
 #if SSSP_PROF
-        for (int i = 0; i < 4; i++) W.prof[i] = 0;
+        for (int i = 0; i < kProf; i++) W.prof[i] = 0;
 #endif
         flush_acc<POL, STATS, FUSE, BIDIR>(p, r, W);
         grid_sync(nullptr);
@@ -1294,7 +1311,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                 t->busy_a_max_ns = (int64_t)C->busy_a_max;
                 t->fused = (int64_t)C->fused;
                 t->t_near_ns = (int64_t)(tn - t0);
-                for (int i = 0; i < 4; i++) t->prof_cyc[i] = (int64_t)C->prof[i];
+                for (int i = 0; i < kProf; i++) t->prof[i] = (int64_t)C->prof[i];
             }
             ctrl->tot_extracted += f;
             ctrl->tot_edges += (int64_t)C->edges;

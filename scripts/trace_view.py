@@ -35,9 +35,11 @@ def main():
                 print(f"{i:4d} q={g('qsize'):9d} qn={g('qnear'):9d} f={g('fsize'):8d} fu={g('fused'):7d} "
                       f"E={g('edges'):10d} th={th:6.1f} near={near:6.1f} A={A:7.1f} ua={ua:.2f} "
                       f"amax={amax:7.1f} B={B:7.1f} heavy={g('nheavy')}"
-                      + (" | per-warp us scan/take/relax/flush " +
-                         " ".join(f"{g(k) / NW / 1.93e3:5.1f}" for k in ("prof_scan", "prof_take", "prof_relax", "prof_flush"))
-                         if g("prof_scan") else ""))
+                      + (" | per-warp us scan/take/relax/flush/fuse " +
+                         " ".join(f"{g(k) / NW / 1.93e3:5.1f}" for k in ("prof_scan", "prof_take", "prof_relax", "prof_flush", "prof_fuse"))
+                         + f" fbatches/w {g('prof_fuse_batches') / NW:5.2f} steps/w {g('prof_steps') / NW:5.2f}"
+                         + f" us/step {g('prof_step_cyc') / max(1, g('prof_steps')) / 1.93e3:5.2f}"
+                         if g("prof_steps") else ""))
         print("totals (us):", {k: round(v, 1) for k, v in tot.items()}, "sum", round(tot["th"] + tot["A"] + tot["B"], 1))
 
 
