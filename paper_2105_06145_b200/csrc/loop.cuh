@@ -69,6 +69,9 @@ constexpr int kWarps = kBlock / 32;
 #ifndef SSSP_PROF
 #define SSSP_PROF 0  // 1: STATS kernels also split phase-A warp time into parts (clock64)
 #endif
+#ifndef SSSP_DYN
+#define SSSP_DYN 1
+#endif
 #ifndef SSSP_NEAR_K
 #define SSSP_NEAR_K 8
 #endif
@@ -97,6 +100,7 @@ constexpr int kSeg = kShards + 1;
 constexpr int kCntStride = 256;              // int32 words between counters (1 KB: distinct L2 slices)
 constexpr int kMaxCtas = 4096;
 constexpr int kPolicies = 5;
+constexpr bool kDyn = SSSP_DYN;               // phase A: dynamic tiles within a CTA share
 constexpr int kProf = 8;                     // SSSP_PROF counters per round
 constexpr int kNearK = SSSP_NEAR_K;          // near queue target: ~kNearK rounds of extraction
 constexpr int kFarSamples = 1024;            // vertices probed to place a new near/far split
@@ -753,7 +757,8 @@ __device__ __forceinline__ void take_batch(const RunParams& p, int32_t cnt, cons
 
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_t>& QC, const int64_t* qpref,
-                                        const Sharded<Desc>& CL, uint64_t theta, bool snap, uint64_t& minrem, Warp& W) {
+                                        const Sharded<Desc>& CL, uint64_t theta, bool snap, uint64_t& minrem, Warp& W,
+                                        int32_t* tile_ctr) {
     const int lane = lane_id();
     const int64_t q = qpref[kSeg];
     const int64_t gw = warp_rank();
@@ -771,7 +776,28 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
     const int64_t lo = contig ? gw * q / nwarps : gw * (32 * ent);
     const int64_t hi = contig ? (gw + 1) * q / nwarps : q;
     const int64_t stride = contig ? 32 * ent : nwarps * (32 * ent);
-    for (int64_t base = lo; base < hi; base += stride) {
+    // SSSP_DYN (kernels without fusion, queues of >= one 32-id tile per warp): the queue
+    // is cut into 32*ent-id tiles dealt to the CTAs round-robin (CTA c owns tiles c,
+    // c + grid, ...: correlated neighbours land on different SMs), and each CTA's warps
+    // take its tiles from a shared-memory counter (no warp idles while its CTA has work).
+    // With fusion, every warp keeps its own thin share: there each warp seeds its own
+    // local search (dynamic tiles left most warps idle and took grid4096 from 932 to
+    // 4,422 rounds).
+    const bool dyn = kDyn && !FUSE && q >= 32 * nwarps;
+    for (int64_t it = 0;; it++) {
+        int64_t base, lim;
+        if (dyn) {
+            int32_t k = 0;
+            if (lane == 0) k = atomicAdd(tile_ctr, 1);
+            k = __shfl_sync(kFull, k, 0);
+            base = ((int64_t)k * gridDim.x + blockIdx.x) * (32 * ent);
+            if (base >= q) break;
+            lim = q;
+        } else {
+            base = lo + it * stride;
+            if (base >= hi) break;
+            lim = hi;
+        }
         PROF_T0(ts);
         int32_t id[kEnt];
         uint64_t val[kEnt];
@@ -780,7 +806,7 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
         for (int e = 0; e < kEnt; e++) {
             const int64_t i = base + e * 32 + lane;
             id[e] = -1;
-            if (e < ent && i < hi) {
+            if (e < ent && i < lim) {
                 int s = sg;
                 while (qpref[s + 1] <= i) s++;
                 id[e] = ld_cg_i32(QC.seg(s) + (i - qpref[s]));
@@ -1013,6 +1039,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     __shared__ int64_t bc_dq;
     __shared__ uint64_t bc_front;
     __shared__ int32_t bc_nl, bc_cnt;
+    __shared__ int32_t tile_ctr[2];      // phase-A tile counters, by round parity
     __shared__ uint64_t red[kWarps];
     Ctrl* ctrl = p.ctrl;
     Warp W;
@@ -1021,6 +1048,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     W.shard = (int)(warp_rank() % kShards);
     W.qn = 0;
     W.fn = 0;
+    if (threadIdx.x == 0) tile_ctr[0] = tile_ctr[1] = 0;
     W.qdelta = 0;
     W.front = 0;
 #if SSSP_PROF
@@ -1095,6 +1123,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         int64_t dense = 0;
         if (STATS && gtid == 0) t0 = tn = globaltimer();
         if (gtid == 0) reset_cnt(&ctrl->cnt[(r + 1) % 3]);
+        if (threadIdx.x == 0) tile_ctr[(r + 1) & 1] = 0;  // last used in round r-1's phase A
         if (gtid < 2 * kSeg) {  // counters of slot (r+1)%3: written in round r+1, read in r+1 / r+2
             p.counters[((int64_t)(((r + 1) % 3) * 2) * kSeg + gtid) * kCntStride] = 0;
         }
@@ -1246,7 +1275,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
 #if SSSP_PROF
         for (int i = 0; i < kProf; i++) W.prof[i] = 0;  // phase-A only
 #endif
-        phase_a<POL, STATS, FUSE, BIDIR>(p, QC, qpref, CL, theta, snap, minrem, W);
+        phase_a<POL, STATS, FUSE, BIDIR>(p, QC, qpref, CL, theta, snap, minrem, W, &tile_ctr[r & 1]);
         if (STATS && lane_id() == 0) {
             const unsigned long long ba = globaltimer() - ta;
             atomicAdd(&C->busy_a, ba);
