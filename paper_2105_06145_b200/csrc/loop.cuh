@@ -1119,7 +1119,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         const Sharded<int32_t> QC = queue_of(p, r);
         const Sharded<Desc> CL = chunks_of(p, r);
         // |Q_r| = |Q_{r-1}| + sum over CTAs of (inserts - extractions) in round r-1
-        if ((threadIdx.x >> 5) == 2 && r > 1) {  // warp 2: the previous round's frontier size and arcs
+        // warps 1-3, in parallel with warp 0's load_prefix: the previous round's |Q| delta,
+        // frontier size and arcs, and min_Q delta (Delta* / Dijkstra)
+        if ((threadIdx.x >> 5) == 2 && r > 1) {
             const int lane = lane_id();
             const int64_t* cf = p.cta_front + ((r + 2) % 3) * kMaxCtas;
             uint64_t sf = 0;
@@ -1127,13 +1129,26 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             sf = warp_sum(sf);
             if (lane == 0) bc_front = sf;
         }
-        if ((threadIdx.x >> 5) == 1 && r > 1) {  // warp 1, in parallel with warp 0's load_prefix
+        if ((threadIdx.x >> 5) == 1 && r > 1) {
             const int lane = lane_id();
             const int64_t* cd = p.cta_delta + ((r + 2) % 3) * kMaxCtas;
             int64_t sdq = 0;
             for (int i = lane; i < (int)gridDim.x; i += 32) sdq += __ldcg((const long long*)(cd + i));
             sdq = warp_sum(sdq);
             if (lane == 0) bc_dq = sdq;
+        }
+        if (uses_min(POL) && FUSE && (threadIdx.x >> 5) == 3) {
+            // (fusion kernels only: in the others this placement cost registers in the hot
+            // loops, rmat24 Delta* +7 %; grid4096 / rgg4m Delta* gain 2 % from it)
+            const int lane = lane_id();
+            const uint64_t* cm = p.cta_min + ((r + 2) % 3) * kMaxCtas;
+            uint64_t mn = kInf;
+            for (int i = lane; i < (int)gridDim.x; i += 32) {
+                const uint64_t x = __ldcg((const unsigned long long*)(cm + i));
+                mn = x < mn ? x : mn;
+            }
+            mn = warp_min_u64(mn);
+            if (lane == 0) bc_u[0] = mn;
         }
         load_prefix(QC, qpref);  // ends with __syncthreads
         if (r > 1) qtot += bc_dq;
@@ -1167,18 +1182,21 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         if (POL == SSSP_BELLMAN_FORD) {
             theta = kInf;
         } else if (POL == SSSP_DIJKSTRA || POL == SSSP_DELTA || POL == SSSP_DELTA_STEPPING) {
-            // min_Q delta = min over the per-CTA minima of the previous round
-            if (threadIdx.x < 32) {
-                const uint64_t* cm = p.cta_min + ((r + 2) % 3) * kMaxCtas;
-                uint64_t mn = kInf;
-                for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) {
-                    const uint64_t x = __ldcg((const unsigned long long*)(cm + i));
-                    mn = x < mn ? x : mn;
+            // min_Q delta = min over the per-CTA minima of the previous round (fusion kernels:
+            // warp 3 above, in parallel with load_prefix)
+            if (!FUSE) {
+                if (threadIdx.x < 32) {
+                    const uint64_t* cm = p.cta_min + ((r + 2) % 3) * kMaxCtas;
+                    uint64_t mn = kInf;
+                    for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) {
+                        const uint64_t x = __ldcg((const unsigned long long*)(cm + i));
+                        mn = x < mn ? x : mn;
+                    }
+                    mn = warp_min_u64(mn);
+                    if (threadIdx.x == 0) bc_u[0] = mn;
                 }
-                mn = warp_min_u64(mn);
-                if (threadIdx.x == 0) bc_u[0] = mn;
+                __syncthreads();
             }
-            __syncthreads();
             const uint64_t minq = bc_u[0];  // <= min_{v in Q} delta[v] (exact in snapshot mode)
             if (POL == SSSP_DIJKSTRA) {
                 theta = minq;
