@@ -46,33 +46,86 @@ __global__ void pq_update_kernel(const int32_t* __restrict__ ids, int64_t count,
     }
 }
 
-__global__ void pq_count_kernel(const int32_t* __restrict__ queue, const uint64_t* __restrict__ keys, uint64_t theta,
-                                PQCtrl* c) {
+__global__ void __launch_bounds__(kPQBlock) pq_count_kernel(const int32_t* __restrict__ queue,
+                                                            const uint64_t* __restrict__ keys, uint64_t theta,
+                                                            PQCtrl* c) {
+    __shared__ int32_t part[kPQBlock / 32];
     const int32_t q = ld_volatile_i32(&c->size);
     int32_t cnt = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += (int64_t)gridDim.x * blockDim.x)
         cnt += ld_cg_u64(keys + queue[i]) <= theta;
     cnt = warp_sum(cnt);
-    if (lane_id() == 0 && cnt) atomicAdd(&c->cnt_out, cnt);
+    if (lane_id() == 0) part[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // one atomic per CTA
+        int32_t t = 0;
+        for (int w = 0; w < kPQBlock / 32; w++) t += part[w];
+        if (t) atomicAdd(&c->cnt_out, t);
+    }
 }
 
-__global__ void pq_extract_kernel(const int32_t* __restrict__ qcur, const uint64_t* __restrict__ keys, uint64_t theta,
-                                  int32_t* out, int32_t* qnext, uint32_t* bm, PQCtrl* c) {
-    const int32_t q = ld_volatile_i32(&c->size);
-    const int lane = lane_id();
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t base = gw * 32; base < q; base += nwarps * 32) {
-        const int64_t i = base + lane;
-        const bool valid = i < q;
-        const int32_t id = valid ? qcur[i] : 0;
-        const bool take = valid && ld_cg_u64(keys + id) <= theta;
-        const bool keep = valid && !take;
-        if (take) atomicAnd(bm + (id >> 5), ~(1u << (id & 31)));
-        const int32_t so = warp_append_slot(take, &c->cnt_out);
-        if (take) out[so] = id;
-        const int32_t sn = warp_append_slot(keep, &c->cnt_next);
-        if (keep) qnext[sn] = id;
+// Extract(theta): CTA tiles of kPQBlock * kPQItems queue entries; the taken and the kept ids
+// of a tile are counted in shared memory and reserved with one atomicAdd each per tile
+// (a per-warp reservation made ~10^5 same-address atomics per call on a 7M queue)
+constexpr int kPQItems = 4;
+__global__ void __launch_bounds__(kPQBlock) pq_extract_kernel(const int32_t* __restrict__ qcur,
+                                                              const uint64_t* __restrict__ keys, uint64_t theta,
+                                                              int32_t* out, int32_t* qnext, uint32_t* bm, PQCtrl* c) {
+    __shared__ int32_t wt[kPQBlock / 32], wk[kPQBlock / 32];  // per-warp take / keep counts
+    __shared__ int32_t base_t, base_k;
+    const int64_t q = ld_volatile_i32(&c->size);
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    constexpr int64_t kTile = (int64_t)kPQBlock * kPQItems;
+    for (int64_t t0 = (int64_t)blockIdx.x * kTile; t0 < q; t0 += (int64_t)gridDim.x * kTile) {
+        int32_t id[kPQItems];
+        bool take[kPQItems], keep[kPQItems];
+#pragma unroll
+        for (int u = 0; u < kPQItems; u++) {  // warp w covers [t0 + w*32*items, ...) in 32-id rows
+            const int64_t i = t0 + ((int64_t)wid * kPQItems + u) * 32 + lane;
+            id[u] = i < q ? qcur[i] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < kPQItems; u++) {
+            take[u] = id[u] >= 0 && ld_cg_u64(keys + id[u]) <= theta;
+            keep[u] = id[u] >= 0 && !take[u];
+        }
+        int32_t nt = 0, nk = 0;
+#pragma unroll
+        for (int u = 0; u < kPQItems; u++) {
+            nt += __popc(__ballot_sync(kFull, take[u]));
+            nk += __popc(__ballot_sync(kFull, keep[u]));
+        }
+        if (lane == 0) {
+            wt[wid] = nt;
+            wk[wid] = nk;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int32_t st = 0, sk = 0;
+            for (int w = 0; w < kPQBlock / 32; w++) {
+                const int32_t a = wt[w], b = wk[w];
+                wt[w] = st;
+                wk[w] = sk;
+                st += a;
+                sk += b;
+            }
+            base_t = st ? atomicAdd(&c->cnt_out, st) : 0;
+            base_k = sk ? atomicAdd(&c->cnt_next, sk) : 0;
+        }
+        __syncthreads();
+        int32_t pt = base_t + wt[wid], pk = base_k + wk[wid];
+#pragma unroll
+        for (int u = 0; u < kPQItems; u++) {
+            const uint32_t mt = __ballot_sync(kFull, take[u]), mk = __ballot_sync(kFull, keep[u]);
+            if (take[u]) {
+                atomicAnd(bm + (id[u] >> 5), ~(1u << (id[u] & 31)));
+                out[pt + __popc(mt & lanemask_lt())] = id[u];
+            }
+            if (keep[u]) qnext[pk + __popc(mk & lanemask_lt())] = id[u];
+            pt += __popc(mt);
+            pk += __popc(mk);
+        }
+        __syncthreads();  // wt / wk / bases are rewritten by the next tile
     }
 }
 
@@ -239,15 +292,21 @@ sssp_status sssp_pq_extract(sssp_pq* q, uint64_t theta, int32_t* d_out, int64_t 
     if (!q || !h_count) return set_error(SSSP_ERR_INVALID, "sssp_pq_extract: NULL argument");
     cudaSetDevice(q->device);
     if (cap < 0 || (cap > 0 && !d_out)) return set_error(SSSP_ERR_INVALID, "sssp_pq_extract: bad output buffer");
-    cudaError_t e = cudaMemsetAsync(&q->ctrl->cnt_out, 0, sizeof(int32_t), q->stream);
-    if (e != cudaSuccess) return cuda_error(e, "sssp_pq_extract");
-    pq_count_kernel<<<q->grid, kPQBlock, 0, q->stream>>>(q->q[q->cur], q->keys, theta, q->ctrl);
+    // the capacity check needs the count before Q changes; a cap >= |Q| cannot overflow, so
+    // then the counting pass is skipped (the size read-back is the only extra step)
     sssp_status s = pq_sync(q, "sssp_pq_extract");
     if (s != SSSP_OK) return s;
-    *h_count = q->h_ctrl->cnt_out;
-    if (q->h_ctrl->cnt_out > cap)
-        return set_error(SSSP_ERR_CAPACITY, "sssp_pq_extract: %d ids qualify, cap %lld", q->h_ctrl->cnt_out,
-                         (long long)cap);
+    if (q->h_ctrl->size > cap) {
+        cudaError_t e = cudaMemsetAsync(&q->ctrl->cnt_out, 0, sizeof(int32_t), q->stream);
+        if (e != cudaSuccess) return cuda_error(e, "sssp_pq_extract");
+        pq_count_kernel<<<q->grid, kPQBlock, 0, q->stream>>>(q->q[q->cur], q->keys, theta, q->ctrl);
+        s = pq_sync(q, "sssp_pq_extract");
+        if (s != SSSP_OK) return s;
+        *h_count = q->h_ctrl->cnt_out;
+        if (q->h_ctrl->cnt_out > cap)
+            return set_error(SSSP_ERR_CAPACITY, "sssp_pq_extract: %d ids qualify, cap %lld", q->h_ctrl->cnt_out,
+                             (long long)cap);
+    }
     cudaMemsetAsync(&q->ctrl->cnt_out, 0, 2 * sizeof(int32_t), q->stream);  // cnt_out, cnt_next
     pq_extract_kernel<<<q->grid, kPQBlock, 0, q->stream>>>(q->q[q->cur], q->keys, theta, d_out, q->q[q->cur ^ 1], q->bm,
                                                            q->ctrl);
