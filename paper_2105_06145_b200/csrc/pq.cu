@@ -145,7 +145,8 @@ __global__ void pq_min_kernel(const int32_t* __restrict__ queue, const uint64_t*
     if (lane_id() == 0 && mn != kInf) atomicMin(&c->minv, (unsigned long long)mn);
 }
 
-// ExtDist of rho-stepping over the queue, one CTA (reading R5/R6, round = 0).
+// ExtDist of rho-stepping over the queue by sampling, one CTA (reading R5/R6,
+// round = 0).
 __global__ void __launch_bounds__(kSelBlock) pq_select_kernel(const int32_t* __restrict__ queue,
                                                               const uint64_t* __restrict__ keys, uint64_t rho,
                                                               uint64_t seed, uint32_t mode, uint64_t* samples,
@@ -155,9 +156,7 @@ __global__ void __launch_bounds__(kSelBlock) pq_select_kernel(const int32_t* __r
     uint64_t th;
     if ((uint64_t)q <= rho) {
         th = kInf;
-    } else if (mode == SSSP_SELECT_EXACT) {
-        th = cta_kth_smallest(QueueKey{queue, keys}, q, rho, sm);
-    } else {
+    } else {  // sampled (the exact mode runs on the whole grid: pq_hist_kernel)
         const uint64_t s = sample_count((uint64_t)q, rho);
         for (uint64_t j = threadIdx.x; j < s; j += blockDim.x) {
             const uint64_t r = splitmix64(seed ^ splitmix64(j));  // round 0: (0 << 32) | j
@@ -171,6 +170,92 @@ __global__ void __launch_bounds__(kSelBlock) pq_select_kernel(const int32_t* __r
     if (threadIdx.x == 0) c->theta = th;
 }
 
+// Exact rho-th smallest over the whole queue with all SMs (SSSP_SELECT_EXACT): MSD radix
+// select, 8 bits per pass over the bits where the queue's min and max keys differ.  Every
+// pass is one grid-wide histogram of the keys that match the current prefix plus a 1-CTA
+// step that picks the bin holding the k-th key; the passes after the answer is known exit
+// at once, so the host enqueues a fixed 8 of them and synchronises once.
+struct SelState {
+    unsigned long long lo, hi;  // min / max key of Q
+    unsigned long long prefix;  // bits above `shift` fixed so far
+    unsigned long long k;       // rank (1-based) within the keys matching prefix
+    int32_t shift;              // bits still open (0 = done)
+    int32_t done;
+    uint32_t hist[256];
+};
+
+__global__ void pq_minmax_kernel(const int32_t* __restrict__ queue, const uint64_t* __restrict__ keys, PQCtrl* c,
+                                 SelState* st) {
+    const int32_t q = ld_volatile_i32(&c->size);
+    uint64_t lo = kInf, hi = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = ld_cg_u64(keys + queue[i]);
+        lo = x < lo ? x : lo;
+        hi = x > hi ? x : hi;
+    }
+    lo = warp_min_u64(lo);
+    hi = warp_max_u64(hi);
+    if (lane_id() == 0) {
+        if (lo != kInf) atomicMin(&st->lo, (unsigned long long)lo);
+        if (hi != 0) atomicMax(&st->hi, (unsigned long long)hi);
+    }
+}
+
+__global__ void pq_sel_init(uint64_t rho, PQCtrl* c, SelState* st) {
+    const int64_t q = c->size;
+    st->done = 1;
+    if ((uint64_t)q <= rho) {
+        c->theta = kInf;  // |Q| <= rho: extract everything
+    } else if (st->lo == st->hi) {
+        c->theta = st->lo;
+    } else {
+        const int top = 63 - __clzll((long long)(st->lo ^ st->hi));  // highest differing bit
+        st->prefix = top == 63 ? 0 : (st->lo >> (top + 1)) << (top + 1);
+        st->shift = top + 1;
+        st->k = rho;
+        st->done = 0;
+    }
+    for (int b = 0; b < 256; b++) st->hist[b] = 0;
+}
+
+__global__ void __launch_bounds__(kPQBlock) pq_hist_kernel(const int32_t* __restrict__ queue,
+                                                           const uint64_t* __restrict__ keys, PQCtrl* c, SelState* st) {
+    __shared__ uint32_t h[256];
+    if (ld_volatile_i32(&st->done)) return;
+    const int32_t q = ld_volatile_i32(&c->size);
+    const int nb = st->shift >= 8 ? 8 : st->shift, sh = st->shift - nb;
+    const uint64_t prefix = st->prefix;
+    const uint64_t above = sh + nb >= 64 ? 0 : ~((1ull << (sh + nb)) - 1);
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = ld_cg_u64(keys + queue[i]);
+        if ((x & above) == prefix) atomicAdd(&h[(x >> sh) & ((1u << nb) - 1)], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < 256; b += blockDim.x)
+        if (h[b]) atomicAdd(&st->hist[b], h[b]);
+}
+
+__global__ void pq_sel_step(PQCtrl* c, SelState* st) {  // one thread
+    if (st->done) return;
+    const int nb = st->shift >= 8 ? 8 : st->shift, sh = st->shift - nb;
+    uint64_t cum = 0;
+    int b = 0;
+    for (; b < (1 << nb) - 1; b++) {
+        if (cum + st->hist[b] >= st->k) break;
+        cum += st->hist[b];
+    }
+    st->k -= cum;
+    st->prefix |= (uint64_t)b << sh;
+    st->shift = sh;
+    for (int i = 0; i < 256; i++) st->hist[i] = 0;
+    if (sh == 0) {
+        st->done = 1;
+        c->theta = st->prefix;
+    }
+}
+
 }  // namespace sssp
 
 using namespace sssp;
@@ -182,6 +267,7 @@ struct sssp_pq {
     int32_t* q[2];
     int cur;
     uint64_t* samples;
+    SelState* sel;
     PQCtrl* ctrl;
     PQCtrl* h_ctrl;
     cudaStream_t stream;
@@ -195,6 +281,7 @@ struct PQLayout {
     uint32_t* bm;
     int32_t *q0, *q1;
     uint64_t* samples;
+    SelState* sel;
     size_t bytes;
 };
 PQLayout pq_carve(void* base, int32_t n) {
@@ -205,6 +292,7 @@ PQLayout pq_carve(void* base, int32_t n) {
     L.q0 = c.take<int32_t>(n);
     L.q1 = c.take<int32_t>(n);
     L.samples = c.take<uint64_t>(kMaxSamples);
+    L.sel = c.take<SelState>(1);
     L.bytes = align_up(c.off, 256);
     return L;
 }
@@ -252,6 +340,7 @@ sssp_status sssp_pq_create(int32_t n, const uint64_t* d_keys, void* d_ws, size_t
     q->q[1] = L.q1;
     q->cur = 0;
     q->samples = L.samples;
+    q->sel = L.sel;
     q->ctrl = L.ctrl;
     q->stream = (cudaStream_t)stream;
     q->grid = sms * 8;
@@ -323,8 +412,21 @@ sssp_status sssp_pq_select(sssp_pq* q, uint64_t rho, uint64_t seed, uint32_t mod
     if (rho == 0) return set_error(SSSP_ERR_INVALID, "sssp_pq_select: rho must be >= 1");
     if (mode != SSSP_SELECT_SAMPLED && mode != SSSP_SELECT_EXACT)
         return set_error(SSSP_ERR_INVALID, "sssp_pq_select: unknown mode %u", mode);
-    pq_select_kernel<<<1, kSelBlock, 0, q->stream>>>(q->q[q->cur], q->keys, rho, seed, mode, q->samples, q->ctrl);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = cudaSuccess;
+    if (mode == SSSP_SELECT_EXACT) {
+        const unsigned long long init[2] = {kInf, 0};  // lo, hi
+        e = cudaMemcpyAsync(q->sel, init, sizeof(init), cudaMemcpyHostToDevice, q->stream);
+        if (e != cudaSuccess) return cuda_error(e, "sssp_pq_select");
+        pq_minmax_kernel<<<q->grid, kPQBlock, 0, q->stream>>>(q->q[q->cur], q->keys, q->ctrl, q->sel);
+        pq_sel_init<<<1, 1, 0, q->stream>>>(rho, q->ctrl, q->sel);
+        for (int pass = 0; pass < 8; pass++) {  // 64-bit keys: at most 8 digits
+            pq_hist_kernel<<<q->grid, kPQBlock, 0, q->stream>>>(q->q[q->cur], q->keys, q->ctrl, q->sel);
+            pq_sel_step<<<1, 1, 0, q->stream>>>(q->ctrl, q->sel);
+        }
+    } else {
+        pq_select_kernel<<<1, kSelBlock, 0, q->stream>>>(q->q[q->cur], q->keys, rho, seed, mode, q->samples, q->ctrl);
+    }
+    e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_error(e, "sssp_pq_select");
     sssp_status s = pq_sync(q, "sssp_pq_select");
     *h_theta = q->h_ctrl->theta;

@@ -121,5 +121,17 @@ def test_select_exact_and_sampled_parity(cuda_device):
             for seed in (0, 99):
                 assert q.select(rho, seed=seed) == oracle.select_sampled(qkeys, rho, seed=seed, round_=0)
         assert q.reduce_min() == int(qkeys.min())
+    # full 64-bit keys: top bit set, SSSP_INF, heavy duplicates (all eight radix digits)
+    for t in range(4):
+        n = 50000
+        pool = np.array([0, 1, 1 << 63, (1 << 64) - 1, (1 << 63) - 1, 12345], dtype=np.uint64)
+        keys_np = np.where(rs.random(n) < 0.5, rs.choice(pool, n), rs.integers(0, 1 << 63, n, dtype=np.uint64) * 2 + 1)
+        keys_np = keys_np.astype(np.uint64)
+        q = P.LabPQ(_keys(keys_np))
+        ids = np.unique(rs.integers(0, n, n)).astype(np.int32)
+        q.update(torch.from_numpy(ids))
+        qkeys = keys_np[q.queue().cpu().numpy()]
+        for rho in (1, 7, len(ids) // 3, len(ids) // 2, len(ids) - 1):
+            assert q.select(rho, exact=True) == oracle.select_exact(qkeys, rho), (t, rho)
     q = P.LabPQ(_keys([1, 2]))
     assert q.reduce_min() == INF and q.select(1) == INF
