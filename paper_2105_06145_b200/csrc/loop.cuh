@@ -488,20 +488,21 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
         cnt += out[t] == kAppend;
         fcnt += out[t] == kFused;
     }
+    static_assert(kArcs < 8, "3-bit per-lane counts");
     if (__any_sync(kFull, cnt != 0)) {
-        const int32_t incl = warp_incl_scan(cnt);
-        const int32_t tot = __shfl_sync(kFull, incl, 31);
+        int32_t tot;
+        const int32_t excl = warp_excl_scan_small<3>(cnt, tot);
         if (W.qn + tot > kQBuf) wq_flush(W);
-        int32_t pos = W.qn + incl - cnt;
+        int32_t pos = W.qn + excl;
 #pragma unroll
         for (int t = 0; t < kArcs; t++)
             if (out[t] == kAppend) W.st->q[pos++] = v[t];
         W.qn += tot;
     }
     if (FUSE && fuse && __any_sync(kFull, fcnt != 0)) {
-        const int32_t incl = warp_incl_scan(fcnt);
-        const int32_t tot = __shfl_sync(kFull, incl, 31);
-        int32_t pos = W.fn + incl - fcnt;
+        int32_t tot;
+        const int32_t excl = warp_excl_scan_small<3>(fcnt, tot);
+        int32_t pos = W.fn + excl;
 #pragma unroll
         for (int t = 0; t < kArcs; t++)
             if (out[t] == kFused) {
@@ -603,9 +604,14 @@ __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, i
             relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W);
         return;
     }
-    const int32_t incl = warp_incl_scan(deg);
-    const int32_t total = __shfl_sync(kFull, incl, 31);
-    const int32_t excl = incl - deg;
+    int32_t total, excl;
+    if (__all_sync(kFull, deg < 64)) {  // light vertices (degree <= 32): bit-plane scan
+        excl = warp_excl_scan_small<6>(deg, total);
+    } else {
+        const int32_t incl = warp_incl_scan(deg);
+        total = __shfl_sync(kFull, incl, 31);
+        excl = incl - deg;
+    }
     const int32_t rowbase = beg - excl;  // CSR position of concatenated arc e of this lane = rowbase + e
     const bool bidir = BIDIR && __any_sync(kFull, uid >= 0);
     for (int32_t s0 = 0; s0 < total; s0 += 32 * kArcs) {
