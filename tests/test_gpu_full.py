@@ -70,3 +70,36 @@ def test_large_id_space(cuda_device):
         got = P.dist_to_u64(h.run(g.source, pol, par))
         assert np.array_equal(got, want), pol
     h.close()
+
+
+TRACE_FIELDS = ["qsize", "fsize", "edges", "inserts", "theta"]
+TRACE_CASES = {
+    "grid256": [("bellman_ford", 0, {}), ("delta", 1 << 13, {}), ("rho", 1 << 10, dict(exact=True))],
+    "rmat20": [("bellman_ford", 0, {}), ("delta", 1 << 15, {}), ("rho", 1 << 15, dict(exact=True)),
+               ("rho", 1 << 15, dict(exact=True, warmup=True))],
+    "rgg4m": [("delta", 1 << 12, {}), ("rho", 1 << 13, dict(exact=True))],
+    "rmat24": [("bellman_ford", 0, {}), ("rho", 1 << 18, dict(exact=True, warmup=True))],
+}
+
+
+@pytest.mark.parametrize("name", list(TRACE_CASES))
+def test_full_round_trace_parity(cuda_device, name):
+    """At the full BASELINE sizes, per-round |Q_r|, |F_r|, E_r, inserts_r and theta_r of the
+    deterministic policies (snapshot rounds, exact rho) equal the oracle's sequential Alg. 1
+    simulation, round by round, and the distances equal its Dijkstra."""
+    import paper_2105_06145_b200 as P
+
+    g = gen.make(name)
+    want = oracle.dijkstra(g)
+    h = P.SSSP.from_graph(g)
+    for pol, par, kw in TRACE_CASES[name]:
+        d, st, tr, _ = h.run(g.source, pol, par, trace_cap=1 << 16, snapshot=True, warmup=kw.get("warmup", False),
+                             exact=kw.get("exact", False))
+        assert np.array_equal(P.dist_to_u64(d), want), (name, pol, par)
+        _, tr_ref, _ = oracle.stepping_sim(g, pol, par, exact=kw.get("exact", True), warmup=kw.get("warmup", False))
+        assert st["rounds"] == len(tr_ref), (name, pol, par, st["rounds"], len(tr_ref))
+        for f in TRACE_FIELDS:
+            if not np.array_equal(tr[f], tr_ref[f]):
+                r = int(np.flatnonzero(tr[f] != tr_ref[f])[0])
+                raise AssertionError(f"{name}/{pol}/{par} round {r + 1} {f}: gpu {tr[f][r]} oracle {tr_ref[f][r]}")
+    h.close()
