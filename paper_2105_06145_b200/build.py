@@ -1,8 +1,9 @@
 """Build libsssp.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
 
-The round-loop kernel template (csrc/loop.cuh) is instantiated per (policy, bidirectional)
-pair: csrc/inst.cu is compiled once per pair with -DINST_POL/-DINST_BIDIR, in parallel with
-the other translation units, and everything is linked into one shared library.
+The round-loop kernel template (csrc/loop.cuh) is instantiated per (policy, bidirectional,
+fusion) triple: csrc/inst.cu is compiled once per triple with -DINST_POL/-DINST_BIDIR/-DINST_FUSE
+(plus UNIT_DEFINES), in parallel with the other translation units, and everything is linked
+into one shared library.
 """
 from __future__ import annotations
 
@@ -22,6 +23,12 @@ NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-
 POLICIES = 5  # SSSP_RHO .. SSSP_DELTA_STEPPING (include/sssp.h)
 
 
+# Unit-specific tuning constants (the constants of csrc/loop.cuh are compile-time): the
+# rho kernels without fusion relax 6 arcs per lane per step (more gathers in flight; the
+# fusion kernels spill with it).  A/B on rmat24: rho = 2^18 -2.6 %, 2^21 -6 %.
+UNIT_DEFINES = {(0, 0, 0): ["-DSSSP_ARCS=6"]}
+
+
 def units():
     """(name, source, extra defines) for every object file of the library."""
     out = [(os.path.splitext(os.path.basename(s))[0], s, []) for s in sorted(glob.glob(os.path.join(CSRC, "*.cu")))
@@ -29,7 +36,10 @@ def units():
     inst = os.path.join(CSRC, "inst.cu")
     for pol in range(POLICIES):
         for bidir in (0, 1):
-            out.append((f"inst_{pol}_{bidir}", inst, [f"-DINST_POL={pol}", f"-DINST_BIDIR={bidir}"]))
+            for fuse in (0, 1):
+                out.append((f"inst_{pol}_{bidir}_{fuse}", inst,
+                            [f"-DINST_POL={pol}", f"-DINST_BIDIR={bidir}", f"-DINST_FUSE={fuse}"]
+                            + UNIT_DEFINES.get((pol, bidir, fuse), [])))
     return out
 
 

@@ -1,20 +1,21 @@
-// inst.cu — explicit instantiation of the round-loop kernels for one policy and one
-// bidirectional setting (INST_POL, INST_BIDIR), compiled once per pair in parallel by build.py.
+// inst.cu — explicit instantiation of the round-loop kernels for one (policy, bidirectional,
+// fusion) triple (INST_POL, INST_BIDIR, INST_FUSE), compiled once per triple in parallel by
+// build.py.  A unit may be compiled with its own tuning constants (build.py UNIT_DEFINES), so
+// it also exports the dynamic shared memory its kernels need.
 #include "loop.cuh"
 
-#ifndef INST_POL
-#error "compile with -DINST_POL=<policy> -DINST_BIDIR=<0|1>"
+#if !defined(INST_POL) || !defined(INST_BIDIR) || !defined(INST_FUSE)
+#error "compile with -DINST_POL=<policy> -DINST_BIDIR=<0|1> -DINST_FUSE=<0|1>"
 #endif
 
 namespace sssp {
 
-#define SSSP_TABLE_NAME2(P, B) kernel_table_##P##_##B
-#define SSSP_TABLE_NAME(P, B) SSSP_TABLE_NAME2(P, B)
+#define SSSP_UNIT_NAME2(X, P, B, F) X##_##P##_##B##_##F
+#define SSSP_UNIT_NAME(X, P, B, F) SSSP_UNIT_NAME2(X, P, B, F)
 
-KernelFn SSSP_TABLE_NAME(INST_POL, INST_BIDIR)(bool stats, bool fuse) {
-    constexpr bool B = INST_BIDIR != 0;
-    if (fuse) return stats ? sssp_round_loop<INST_POL, true, true, B> : sssp_round_loop<INST_POL, false, true, B>;
-    return stats ? sssp_round_loop<INST_POL, true, false, B> : sssp_round_loop<INST_POL, false, false, B>;
+KernelUnit SSSP_UNIT_NAME(kernel_unit, INST_POL, INST_BIDIR, INST_FUSE)() {
+    constexpr bool B = INST_BIDIR != 0, F = INST_FUSE != 0;
+    return KernelUnit{sssp_round_loop<INST_POL, false, F, B>, sssp_round_loop<INST_POL, true, F, B>, smem_bytes(F)};
 }
 
 }  // namespace sssp

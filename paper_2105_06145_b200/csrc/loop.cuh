@@ -1410,13 +1410,20 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
 
 typedef void (*KernelFn)(RunParams);
 
-constexpr size_t smem_bytes(bool fuse) { return kSmemBase + (fuse ? kWarps * sizeof(FuseStage) : 0); }
+// this translation unit's dynamic shared memory per CTA (its constants may be unit-specific)
+static constexpr size_t smem_bytes(bool fuse) { return kSmemBase + (fuse ? kWarps * sizeof(FuseStage) : 0); }
 
-// Kernel tables, one per (policy, bidirectional) object file (inst.cu); mode bit 0 = fusion.
-#define SSSP_DECLARE_TABLE(P, B) KernelFn kernel_table_##P##_##B(bool stats, bool fuse);
-SSSP_DECLARE_TABLE(0, 0) SSSP_DECLARE_TABLE(0, 1) SSSP_DECLARE_TABLE(1, 0) SSSP_DECLARE_TABLE(1, 1)
-SSSP_DECLARE_TABLE(2, 0) SSSP_DECLARE_TABLE(2, 1) SSSP_DECLARE_TABLE(3, 0) SSSP_DECLARE_TABLE(3, 1)
-SSSP_DECLARE_TABLE(4, 0) SSSP_DECLARE_TABLE(4, 1)
-#undef SSSP_DECLARE_TABLE
+// One object file (inst.cu) per (policy, bidirectional, fusion): the plain and the stats
+// kernel and the shared memory they need.
+struct KernelUnit {
+    KernelFn plain, stats;
+    size_t smem;
+};
+#define SSSP_DECLARE_UNIT(P, B, F) KernelUnit kernel_unit_##P##_##B##_##F();
+#define SSSP_DECLARE_UNITS(P) \
+    SSSP_DECLARE_UNIT(P, 0, 0) SSSP_DECLARE_UNIT(P, 0, 1) SSSP_DECLARE_UNIT(P, 1, 0) SSSP_DECLARE_UNIT(P, 1, 1)
+SSSP_DECLARE_UNITS(0) SSSP_DECLARE_UNITS(1) SSSP_DECLARE_UNITS(2) SSSP_DECLARE_UNITS(3) SSSP_DECLARE_UNITS(4)
+#undef SSSP_DECLARE_UNITS
+#undef SSSP_DECLARE_UNIT
 
 }  // namespace sssp

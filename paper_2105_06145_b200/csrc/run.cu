@@ -90,7 +90,8 @@ Layout carve(void* base, int32_t n, int64_t m) {
     // queue: kShards segments of qcap (2x the even share + slack) plus a spill segment of n
     L.qcap = 2 * (((int64_t)n + kShards - 1) / kShards) + 1024;
     const int64_t qlen = kShards * L.qcap + n;
-    // chunks per round <= sum over heavy extracted vertices of ceil(deg/kChunk)
+    // chunks per round <= sum over heavy extracted vertices of ceil(deg/kChunk); kernel units
+    // built with more arcs per lane (build.py UNIT_DEFINES) cut longer chunks, i.e. fewer
     const int64_t ctot = m / kChunk + std::min<int64_t>(n, m / (kLight + 1)) + 1;
     L.ccap = 2 * ((ctot + kShards - 1) / kShards) + 256;
     L.cspill = ctot;
@@ -114,16 +115,24 @@ Layout carve(void* base, int32_t n, int64_t m) {
 }
 
 
-KernelFn kernel_for(int pol, bool stats, int mode) {
-    const bool fuse = mode & 1, bidir = mode & 2;
+KernelUnit unit_for(int pol, int mode) {
+    const int fuse = mode & 1, bidir = (mode >> 1) & 1;
+#define SSSP_UNIT_CASE(P) \
+    case P:               \
+        return bidir ? (fuse ? kernel_unit_##P##_1_1() : kernel_unit_##P##_1_0()) : (fuse ? kernel_unit_##P##_0_1() : kernel_unit_##P##_0_0());
     switch (pol) {
-        case SSSP_RHO: return bidir ? kernel_table_0_1(stats, fuse) : kernel_table_0_0(stats, fuse);
-        case SSSP_DELTA: return bidir ? kernel_table_1_1(stats, fuse) : kernel_table_1_0(stats, fuse);
-        case SSSP_BELLMAN_FORD: return bidir ? kernel_table_2_1(stats, fuse) : kernel_table_2_0(stats, fuse);
-        case SSSP_DIJKSTRA: return bidir ? kernel_table_3_1(stats, fuse) : kernel_table_3_0(stats, fuse);
-        case SSSP_DELTA_STEPPING: return bidir ? kernel_table_4_1(stats, fuse) : kernel_table_4_0(stats, fuse);
+        SSSP_UNIT_CASE(0)
+        SSSP_UNIT_CASE(1)
+        SSSP_UNIT_CASE(2)
+        SSSP_UNIT_CASE(3)
+        SSSP_UNIT_CASE(4)
     }
-    return nullptr;
+#undef SSSP_UNIT_CASE
+    return KernelUnit{nullptr, nullptr, 0};
+}
+KernelFn kernel_for(int pol, bool stats, int mode) {
+    const KernelUnit u = unit_for(pol, mode);
+    return stats ? u.stats : u.plain;
 }
 
 
@@ -160,7 +169,8 @@ sssp_status launch_run(sssp_handle* h, int32_t source, sssp_policy policy, uint6
     KernelFn k = kernel_for(policy, st, mode);
     const int grid = h->grid[policy][st][mode];
     void* args[] = {&p};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kBlock), args, smem_bytes(fu), h->stream);
+    cudaError_t e =
+        cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kBlock), args, unit_for(policy, mode).smem, h->stream);
     if (e != cudaSuccess) return cuda_error(e, "round-loop launch");
     *grid_out = grid;
     *max_rounds_out = p.max_rounds;
@@ -245,11 +255,12 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
         for (int st = 0; st < 2; st++)
             for (int sn = 0; sn < 4; sn++) {  // mode: bit 0 fusion, bit 1 bidirectional
                 int per_sm = 0;
+                const size_t smem = unit_for(pol, sn).smem;
                 e = cudaFuncSetAttribute((const void*)kernel_for(pol, st, sn),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(sn & 1));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 if (e == cudaSuccess)
                     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kernel_for(pol, st, sn),
-                                                                      kBlock, smem_bytes(sn & 1));
+                                                                      kBlock, smem);
                 if (e != cudaSuccess || per_sm < 1) {
                     delete h;
                     return e != cudaSuccess ? cuda_error(e, "occupancy query")
