@@ -29,8 +29,11 @@ POLICIES = 5  # SSSP_RHO .. SSSP_DELTA_STEPPING (include/sssp.h)
 UNIT_DEFINES = {(0, 0, 0): ["-DSSSP_ARCS=6"]}
 
 
-def units():
+def units(unit_defines=None):
     """(name, source, extra defines) for every object file of the library."""
+    ud = {k: list(v) for k, v in UNIT_DEFINES.items()}
+    for k, v in (unit_defines or {}).items():
+        ud[k] = ud.get(k, []) + list(v)
     out = [(os.path.splitext(os.path.basename(s))[0], s, []) for s in sorted(glob.glob(os.path.join(CSRC, "*.cu")))
            if os.path.basename(s) != "inst.cu"]
     inst = os.path.join(CSRC, "inst.cu")
@@ -39,7 +42,7 @@ def units():
             for fuse in (0, 1):
                 out.append((f"inst_{pol}_{bidir}_{fuse}", inst,
                             [f"-DINST_POL={pol}", f"-DINST_BIDIR={bidir}", f"-DINST_FUSE={fuse}"]
-                            + UNIT_DEFINES.get((pol, bidir, fuse), [])))
+                            + ud.get((pol, bidir, fuse), [])))
     return out
 
 
@@ -55,10 +58,11 @@ def up_to_date(out: str = OUT) -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=()) -> str:
+def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=(), unit_defines=None) -> str:
     """Compile every translation unit (in parallel) and link the shared library.
-    defines: tuning variants, e.g. SSSP_ARCS=4 (written to a separate `out`)."""
-    if not force and out == OUT and not defines and up_to_date():
+    defines: tuning variants for every unit, e.g. SSSP_ARCS=4; unit_defines: {(pol, bidir,
+    fuse): ["-DNAME=VAL", ...]} added to one unit (both written to a separate `out`)."""
+    if not force and out == OUT and not defines and not unit_defines and up_to_date():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
     tag = os.path.splitext(os.path.basename(out))[0]
@@ -77,7 +81,7 @@ def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=())
 
     jobs = int(os.environ.get("SSSP_BUILD_JOBS", str(os.cpu_count() or 4)))
     with ThreadPoolExecutor(max_workers=max(1, jobs)) as ex:
-        results = list(ex.map(compile_one, units()))
+        results = list(ex.map(compile_one, units(unit_defines)))
     log_path = os.path.join(HERE, "build.log" if out == OUT else os.path.basename(out) + ".log")
     with open(log_path, "w") as log:
         for name, obj, cmd, res in results:
@@ -98,9 +102,14 @@ def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=())
 
 
 if __name__ == "__main__":
-    # python build.py [--force] [--out lib.so] [-DNAME=VAL ...]
+    # python build.py [--force] [--out lib.so] [-DNAME=VAL ...] [--unit P,B,F:NAME=VAL ...]
     args = sys.argv[1:]
     out = OUT
     if "--out" in args:
         out = os.path.abspath(args[args.index("--out") + 1])
-    build(force="--force" in args, out=out, defines=[a[2:] for a in args if a.startswith("-D")])
+    ud = {}
+    for i, a in enumerate(args):
+        if a == "--unit":
+            key, d = args[i + 1].split(":")
+            ud.setdefault(tuple(int(x) for x in key.split(",")), []).append("-D" + d)
+    build(force="--force" in args, out=out, defines=[a[2:] for a in args if a.startswith("-D")], unit_defines=ud)
