@@ -1,6 +1,7 @@
 // loop.cuh — the stepping-algorithm round loop (Alg. 1) as ONE persistent
-// cooperative kernel template.  Included by inst.cu (compiled once per policy and
-// bidirectional flag, in parallel) and by run.cu (host API: layout and launch only).
+// cooperative kernel template.  Included by inst.cu (compiled once per policy,
+// bidirectional flag and fusion flag, in parallel, possibly with unit-specific constants)
+// and by run.cu (host API: layout and launch only).
 //
 // LaB-PQ of the round loop: the membership flag of a vertex lives in
 // the top bit of its delta word (bit 63 set = NOT in Q), the value in the low 63
@@ -24,14 +25,17 @@
 //   ExtDist  theta_r per policy (Table tab:framework).  rho: every CTA
 //            draws the same counter-based samples into shared memory and selects
 //            the same theta (readings R5/R6) -> no barrier.
-//   Phase A  one pass over the queue (array LaB-PQ P:1011-1012): ids with
-//            key <= theta are extracted; vertices of degree <= kLight are relaxed by
-//            the extracting warp (live) or listed (snapshot mode); heavier ones are
-//            cut into kChunk-arc descriptors; the rest of Q is compacted into the
-//            next queue.                                              grid barrier
+//   Phase A  one pass over the queue (array LaB-PQ P:1011-1012) in tiles
+//            (dealt to CTAs, taken by warps from a shared-memory counter; one thin
+//            share per warp in fusion kernels): ids with key <= theta are extracted;
+//            vertices of degree <= kLight are relaxed by the extracting warp (live) or
+//            listed (snapshot mode); heavier ones are cut into kChunk-arc descriptors;
+//            the rest of Q is compacted into the next queue.  In live rounds of sparse
+//            graphs a WriteMin that reaches a vertex outside Q within theta extracts it
+//            on the spot (fusion).                      grid barrier
 //   Phase B  warps stride over the chunk descriptors (and, in snapshot mode, the
-//            light list): per arc c = d_u + w, plain L2 load filter, WriteMin by CAS
-//            (P:697), append on insertion.          grid barrier (only if non-empty)
+//            light list): per arc c = d_u + w, filter load of delta[v] (through L1),
+//            WriteMin by CAS, append on insertion.  grid barrier (if non-empty)
 //   loop while |Q| > 0.
 #pragma once
 #include <stdio.h>
@@ -103,7 +107,7 @@ constexpr int kSeg = kShards + 1;
 constexpr int kCntStride = 256;              // int32 words between counters (1 KB: distinct L2 slices)
 constexpr int kMaxCtas = 4096;
 constexpr int kPolicies = 5;
-constexpr bool kDyn = SSSP_DYN;               // phase A: dynamic tiles within a CTA share
+constexpr bool kDyn = SSSP_DYN;               // phase A: tiles dealt to CTAs, taken by warps dynamically
 constexpr int kProf = 8;                     // SSSP_PROF counters per round
 constexpr int kNearK = SSSP_NEAR_K;          // near queue target: ~kNearK rounds of extraction
 constexpr int kFarSamples = 1024;            // vertices probed to place a new near/far split
