@@ -1340,6 +1340,18 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         for (int i = 0; i < kProf; i++) W.prof[i] = 0;
 #endif
         flush_acc<POL, STATS, FUSE, BIDIR>(p, r, W);
+        // this CTA's min over kept ids and successful WriteMins so far (Delta* / Dijkstra):
+        // published before the barrier, so a round without phase-B work needs no second one
+        auto publish_min = [&]() {
+            uint64_t mn = warp_min_u64(minrem < W.acc.minsucc ? minrem : W.acc.minsucc);
+            if (lane_id() == 0) red[threadIdx.x >> 5] = mn;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int i = 1; i < kWarps; i++) mn = red[i] < mn ? red[i] : mn;
+                p.cta_min[(r % 3) * kMaxCtas + blockIdx.x] = mn;
+            }
+        };
+        if (uses_min(POL)) publish_min();
         grid_sync(nullptr);
         if (STATS && gtid == 0) t2 = globaltimer();
         // ---- phase B: heavy chunks (+ light list in snapshot mode)
@@ -1353,20 +1365,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             phase_b<POL, STATS, FUSE, BIDIR>(p, CL, cpref, nl, W);
             if (STATS && lane_id() == 0) atomicAdd(&C->busy_b, (unsigned long long)(globaltimer() - tb));
         }
-        if (uses_min(POL)) {  // this CTA's min over kept ids and successful WriteMins
-            uint64_t mn = warp_min_u64(minrem < W.acc.minsucc ? minrem : W.acc.minsucc);
-            if (lane_id() == 0) red[threadIdx.x >> 5] = mn;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                for (int i = 1; i < kWarps; i++) mn = red[i] < mn ? red[i] : mn;
-                p.cta_min[(r % 3) * kMaxCtas + blockIdx.x] = mn;
-            }
+        if (uses_min(POL)) {
+            if (phase_b_work) publish_min();  // now including phase B's WriteMins
             W.acc.minsucc = kInf;
         }
         if (phase_b_work) {
             flush_acc<POL, STATS, FUSE, BIDIR>(p, r, W);
             grid_sync(nullptr);
-        } else if (uses_min(POL) || STATS) {
+        } else if (STATS) {
             grid_sync(nullptr);
         }
         if (STATS && gtid == 0) t3 = globaltimer();
