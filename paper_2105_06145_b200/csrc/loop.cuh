@@ -110,7 +110,11 @@ constexpr int kPolicies = 5;
 constexpr bool kDyn = SSSP_DYN;               // phase A: tiles dealt to CTAs, taken by warps dynamically
 constexpr int kProf = 8;                     // SSSP_PROF counters per round
 constexpr int kNearK = SSSP_NEAR_K;          // near queue target: ~kNearK rounds of extraction
-constexpr int kFarSamples = 1024;            // vertices probed to place a new near/far split
+#ifndef SSSP_FAR_SAMPLES
+#define SSSP_FAR_SAMPLES 256
+#endif
+constexpr int kFarSamples = SSSP_FAR_SAMPLES; // vertices probed to place a new near/far split (<= kRankSelect
+                                              // far keys: a rank-count select, no radix passes)
 static_assert(32 * kArcs <= kQBuf, "one relax step must fit the stage");
 static_assert(kBlock % 32 == 0 && kBlock <= 1024, "block size");
 
