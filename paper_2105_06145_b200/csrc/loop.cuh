@@ -68,7 +68,10 @@ constexpr int kArcs = SSSP_ARCS;             // arcs per lane in flight
 constexpr int kChunk = 32 * kArcs;           // arcs per heavy-chunk descriptor
 constexpr int kLight = SSSP_LIGHT;           // out-degree <= kLight: relaxed by the extracting warp
 constexpr int kSmemSamples = 2048;           // theta samples held in shared memory (else CTA-0 fallback)
-constexpr int kRankSelect = 256;             // s <= this: select by rank counting
+#ifndef SSSP_RANK_SELECT
+#define SSSP_RANK_SELECT 256
+#endif
+constexpr int kRankSelect = SSSP_RANK_SELECT;  // s <= this: select by rank counting
 constexpr int kWarps = kBlock / 32;
 #ifndef SSSP_PROF
 #define SSSP_PROF 0  // 1: STATS kernels also split phase-A warp time into parts (clock64)
