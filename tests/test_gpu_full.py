@@ -103,3 +103,30 @@ def test_full_round_trace_parity(cuda_device, name):
                 r = int(np.flatnonzero(tr[f] != tr_ref[f])[0])
                 raise AssertionError(f"{name}/{pol}/{par} round {r + 1} {f}: gpu {tr[f][r]} oracle {tr_ref[f][r]}")
     h.close()
+
+
+OPTION_CASES = {
+    # run options off the default path, at full size: bidirectional relaxation (all five
+    # configs are undirected), other fusion budgets and no fusion, the near/far queue off,
+    # snapshot rounds with sampled rho
+    "rgg4m": [("delta", 1 << 12, dict(bidir=True)), ("delta", 1 << 13, dict(fuse_budget=256)),
+              ("delta", 1 << 12, dict(fuse=False)), ("rho", 1 << 13, dict(nearfar=False))],
+    "grid4096": [("delta", 1 << 17, dict(bidir=True)), ("delta", 1 << 18, dict(fuse_budget=256))],
+    "rmat24": [("rho", 1 << 18, dict(nearfar=False)), ("rho", 1 << 18, dict(bidir=True)),
+               ("rho", 1 << 18, dict(snapshot=True)), ("delta", 1 << 17, dict(bidir=True))],
+}
+
+
+@pytest.mark.parametrize("name", list(OPTION_CASES))
+def test_full_options(cuda_device, name):
+    import paper_2105_06145_b200 as P
+
+    g = gen.make(name)
+    want = oracle.dijkstra(g)
+    h = P.SSSP.from_graph(g)
+    for pol, par, kw in OPTION_CASES[name]:
+        got = P.dist_to_u64(h.run(g.source, pol, par, **kw))
+        if not np.array_equal(got, want):
+            bad = np.flatnonzero(got != want)
+            raise AssertionError(f"{name}/{pol}/{par}/{kw}: {len(bad)} mismatches, first {bad[0]}")
+    h.close()
