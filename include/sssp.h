@@ -74,6 +74,12 @@ typedef struct sssp_handle sssp_handle;
 
 /* sssp_create flags */
 #define SSSP_VALIDATE 1u /* check the CSR on the device at create time (one extra kernel) */
+#define SSSP_NO_RELABEL 2u /* keep the caller's vertex ids inside the handle.  By default a
+                            * power-law graph (m >= 20 n) with >= n/16 isolated vertices is
+                            * renumbered inside the handle: the non-isolated vertices become
+                            * 0..nz-1 (original order), so the run's distance array holds
+                            * only them; runs map the source in and the distances back, the
+                            * API is unchanged (workspace +20n bytes when m >= 20 n) */
 
 /* Bytes of device workspace a handle for an n-vertex, m-arc graph needs (flags as
  * for sssp_create).  Holds an interleaved copy of the arcs ({head, weight}, 8m

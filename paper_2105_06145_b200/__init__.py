@@ -31,6 +31,7 @@ SSSP_RHO, SSSP_DELTA, SSSP_BELLMAN_FORD, SSSP_DIJKSTRA, SSSP_DELTA_STEPPING = 0,
 POLICIES = {"rho": SSSP_RHO, "delta": SSSP_DELTA, "bellman_ford": SSSP_BELLMAN_FORD, "bf": SSSP_BELLMAN_FORD,
             "dijkstra": SSSP_DIJKSTRA, "delta_stepping": SSSP_DELTA_STEPPING}
 SSSP_VALIDATE = 1
+SSSP_NO_RELABEL = 2
 SSSP_RUN_RHO_EXACT, SSSP_RUN_NO_WARMUP, SSSP_RUN_STATS, SSSP_RUN_SNAPSHOT, SSSP_RUN_NO_NEARFAR = 1, 2, 4, 8, 16
 SSSP_RUN_NO_FUSE, SSSP_RUN_BIDIR = 32, 64
 SSSP_SELECT_SAMPLED, SSSP_SELECT_EXACT = 0, 1
@@ -126,7 +127,7 @@ def _ptr(t):
 class SSSP:
     """Handle over a device-resident CSR (int32 offsets/indices, uint32 weights as int32 or uint32 tensors)."""
 
-    def __init__(self, offsets, indices, weights, validate: bool = False, stream=None):
+    def __init__(self, offsets, indices, weights, validate: bool = False, stream=None, relabel: bool = True):
         torch = _torch()
         if not torch.cuda.is_available():
             raise RuntimeError("SSSP needs a CUDA device (no CPU fallback)")
@@ -138,7 +139,7 @@ class SSSP:
         self.m = indices.numel()
         self.offsets, self.indices, self.weights = offsets, indices, weights  # keep borrowed buffers alive
         self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
-        flags = SSSP_VALIDATE if validate else 0
+        flags = (SSSP_VALIDATE if validate else 0) | (0 if relabel else SSSP_NO_RELABEL)
         nbytes = sssp_workspace_bytes(self.n, self.m, flags)
         if nbytes == 0:
             raise ValueError(f"graph size out of range (n={self.n}, m={self.m})")
@@ -151,13 +152,13 @@ class SSSP:
         self._h = h
 
     @staticmethod
-    def from_graph(g, device="cuda", validate=False):
+    def from_graph(g, device="cuda", validate=False, relabel=True):
         """Upload a host CSR (gen.Graph or anything with offsets/indices/weights numpy arrays)."""
         torch = _torch()
         off = torch.from_numpy(g.offsets).to(device)
         idx = torch.from_numpy(g.indices).to(device)
         w = torch.from_numpy(g.weights.view("int32")).to(device)
-        return SSSP(off, idx, w, validate=validate)
+        return SSSP(off, idx, w, validate=validate, relabel=relabel)
 
     def run(self, source, policy="rho", param=0, out=None, stats=False, trace_cap=0, ext_counts=False,
             exact=False, warmup=True, seed=0, max_rounds=0, snapshot=False, nearfar=True, fuse=True,

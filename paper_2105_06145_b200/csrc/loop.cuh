@@ -176,6 +176,14 @@ struct RunParams {
     int64_t m;
     const int32_t* __restrict__ off;
     const uint2* __restrict__ arc;  // interleaved CSR arcs {head, weight} (workspace copy)
+    // isolated-vertex compaction (run.cu build_compaction): the run works on ids 0..n-1
+    // (the non-isolated vertices); nofo / ofno map caller ids <-> run ids, `out` is the
+    // caller's distance array of n_out entries.  nofo == nullptr: no compaction, dist is
+    // the caller's array
+    const int32_t* nofo;
+    const int32_t* ofno;
+    uint64_t* out;
+    int32_t n_out;
     uint64_t* dist;
     int32_t* qbuf[2];   // queue storage, ping-pong
     int64_t qcap;       // per-shard queue capacity
@@ -696,7 +704,7 @@ __device__ __forceinline__ void fuse_drain(const RunParams& p, Warp& W) {
         }
         wq_push1(W, back, hub);
         if (id >= 0) {
-            if (p.ext_count) atomicAdd(p.ext_count + id, 1);
+            if (p.ext_count) atomicAdd(p.ext_count + (p.ofno ? p.ofno[id] : id), 1);
             W.front += 1 | ((uint64_t)deg << 32);
             if (STATS) {
                 W.acc.fused++;  // counted as inserted and extracted (the |Q| identity holds)
@@ -774,7 +782,7 @@ __device__ __forceinline__ void take_batch(const RunParams& p, int32_t cnt, cons
         W.qdelta--;
         W.front += 1;
         W.front += (uint64_t)deg << 32;
-        if (p.ext_count) atomicAdd(p.ext_count + id, 1);
+        if (p.ext_count) atomicAdd(p.ext_count + (p.ofno ? p.ofno[id] : id), 1);
     }
     if (STATS && id >= 0) {
         fs += 1;
@@ -1099,9 +1107,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
 
     // Alg. 1 lines 1-2: delta[.] = +inf (not in Q), delta[s] = 0 (in Q), Q_1 = {s}
-    for (int64_t i = gtid; i < p.n; i += gsize) p.dist[i] = (i == p.source) ? 0ull : kInf;
+    // the source in run ids (an isolated source of a compacted graph lies past p.n: it is
+    // extracted in round 1 and relaxes nothing)
+    const int32_t src = p.nofo ? p.nofo[p.source] : p.source;
+    for (int64_t i = gtid; i < p.n; i += gsize) p.dist[i] = (i == src) ? 0ull : kInf;
+    if (gtid == 0 && src >= p.n) p.dist[src] = 0;
     if (p.ext_count)
-        for (int64_t i = gtid; i < p.n; i += gsize) p.ext_count[i] = 0;
+        for (int64_t i = gtid; i < (p.nofo ? p.n_out : p.n); i += gsize) p.ext_count[i] = 0;
     for (int64_t i = gtid; i < 3 * 2 * kSeg; i += gsize) p.counters[i * kCntStride] = 0;
     for (int64_t i = gtid; i < 3 * kMaxCtas; i += gsize) {
         p.cta_min[i] = kInf;
@@ -1109,7 +1121,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         p.cta_front[i] = 0;
     }
     if (gtid == 0) {
-        p.qbuf[1][0] = p.source;  // Q_1 lives in qbuf[1], shard 0
+        p.qbuf[1][0] = src;  // Q_1 lives in qbuf[1], shard 0
         for (int c = 0; c < 3; c++) reset_cnt(&ctrl->cnt[c]);
         ctrl->status = 0;
         ctrl->rounds = 0;
@@ -1419,9 +1431,17 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     }
     if (gtid == 0) ctrl->rounds = r - 1;
     // S6 output: strip the flag bit (every reached vertex was extracted; INF stays INF)
-    for (int64_t i = gtid; i < p.n; i += gsize) {
-        const uint64_t x = __ldcg((const unsigned long long*)(p.dist + i));
-        if (x != kInf && (x & kTop)) p.dist[i] = x & kVal;
+    if (p.nofo) {  // compacted ids: out[v] = delta[nofo[v]] for every caller id v
+        for (int64_t v = gtid; v < p.n_out; v += gsize) {
+            const int32_t u = p.nofo[v];
+            const uint64_t x = (u < p.n || u == src) ? __ldcg((const unsigned long long*)(p.dist + u)) : kInf;
+            p.out[v] = (x != kInf && (x & kTop)) ? (x & kVal) : x;
+        }
+    } else {
+        for (int64_t i = gtid; i < p.n; i += gsize) {
+            const uint64_t x = __ldcg((const unsigned long long*)(p.dist + i));
+            if (x != kInf && (x & kTop)) p.dist[i] = x & kVal;
+        }
     }
 }
 

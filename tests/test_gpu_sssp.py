@@ -314,3 +314,29 @@ def test_unaligned_output_buffer(cuda_device):
             _, st, _, _ = h.run(g.source, "rho", par, out=out, stats=True)
             assert st["dense_scanned"] > 0  # the dense pass ran
             _assert_same(P.dist_to_u64(out), want, f"offset {off}/rho {par}/stats")
+
+
+def test_isolated_vertex_compaction(cuda_device):
+    """Power-law graphs with many isolated vertices are renumbered inside the handle (the
+    non-isolated ones become 0..nz-1); sources map in and distances / extraction counts map
+    back, so results are identical with the compaction on and off, for isolated and
+    non-isolated sources."""
+    P = _P()
+    g = gen.make("rmat14log")
+    deg = np.diff(g.offsets.astype(np.int64))
+    iso = np.flatnonzero(deg == 0)
+    assert g.m >= 20 * g.n and len(iso) >= g.n // 16  # compaction applies
+    nz = np.flatnonzero(deg > 0)
+    h_on = P.SSSP.from_graph(g)
+    h_off = P.SSSP.from_graph(g, relabel=False)
+    assert h_on.workspace.numel() > h_off.workspace.numel()
+    for s in [int(g.source), int(nz[len(nz) // 2]), int(nz[-1]), int(iso[0]), int(iso[-1])]:
+        want = oracle.dijkstra(g, source=s)
+        for pol, par, kw in (("rho", 256, {}), ("delta", 1 << 14, {}), ("bellman_ford", 0, dict(snapshot=True))):
+            d_on, st_on, _, e_on = h_on.run(s, pol, par, ext_counts=True, stats=True, **kw)
+            d_off, st_off, _, e_off = h_off.run(s, pol, par, ext_counts=True, stats=True, **kw)
+            _assert_same(P.dist_to_u64(d_on), want, f"compaction on s={s} {pol}")
+            _assert_same(P.dist_to_u64(d_off), want, f"compaction off s={s} {pol}")
+            if kw.get("snapshot"):  # deterministic rounds: identical extraction counts per vertex
+                _assert_same(e_on.cpu().numpy(), e_off.cpu().numpy(), f"ext counts s={s}")
+                assert st_on["rounds"] == st_off["rounds"]
