@@ -174,7 +174,9 @@ typedef struct {
 /* Single-source shortest paths from `source` with the given policy (Alg. 1).
  *   d_dist_out: caller-owned device uint64[n]; receives the exact distances
  *   (SSSP_INF if unreachable).  Also used as the live tentative-distance array
- *   delta during the run.  stats: nullable host struct.
+ *   delta during the run, unless the handle compacted isolated vertices (see
+ *   SSSP_NO_RELABEL): then delta is in the workspace and the last pass of the run
+ *   writes every entry of d_dist_out.  stats: nullable host struct.
  * The whole run is ONE persistent cooperative kernel launch on the handle's
  * stream; the call then synchronises the stream to report device-side status.
  * Errors: SSSP_ERR_RANGE (source outside [0,n)), SSSP_ERR_INVALID (param == 0 for
