@@ -26,7 +26,10 @@ POLICIES = 5  # SSSP_RHO .. SSSP_DELTA_STEPPING (include/sssp.h)
 # Unit-specific tuning constants (the constants of csrc/loop.cuh are compile-time): the
 # rho kernels without fusion relax 6 arcs per lane per step (more gathers in flight; the
 # fusion kernels spill with it).  A/B on rmat24: rho = 2^18 -2.6 %, 2^21 -6 %.
-UNIT_DEFINES = {(0, 0, 0): ["-DSSSP_ARCS=6"]}
+# The segment hint in phase B (forward scan instead of a binary search per descriptor)
+# helps BF / Delta* by ~2 % and costs the 6-arc rho unit ~2 % (register allocation), so
+# that unit keeps the binary search.
+UNIT_DEFINES = {(0, 0, 0): ["-DSSSP_ARCS=6", "-DSSSP_SEG_HINT=0"]}
 
 
 def units(unit_defines=None):

@@ -82,6 +82,9 @@ constexpr int kWarps = kBlock / 32;
 #ifndef SSSP_LANE_LOCAL
 #define SSSP_LANE_LOCAL 1  // relax batches whose degrees are all <= kArcs lane-locally
 #endif
+#ifndef SSSP_SEG_HINT
+#define SSSP_SEG_HINT 1  // phase B: find a descriptor's segment by a forward scan from the last one
+#endif
 #ifndef SSSP_NEAR_K
 #define SSSP_NEAR_K 8
 #endif
@@ -915,9 +918,14 @@ __device__ __forceinline__ void phase_b(const RunParams& p, const Sharded<Desc>&
     const int64_t nb = ((int64_t)nl + 31) / 32;
     const int64_t nc = cpref[kSeg];
     const int64_t total = nb + nc;
+    int sh = 0;  // SSSP_SEG_HINT: segment of the last descriptor read (a warp's items only increase)
     auto chunk_at = [&](int64_t i) {  // i-th descriptor of the concatenated segments
-        const int s = seg_of(cpref, i);
-        return ld_desc(CL.seg(s) + (i - cpref[s]));
+        if (SSSP_SEG_HINT) {
+            while (sh < kShards && cpref[sh + 1] <= i) sh++;
+        } else {
+            sh = seg_of(cpref, i);
+        }
+        return ld_desc(CL.seg(sh) + (i - cpref[sh]));
     };
     int64_t item = gw;
     Desc nxt;
