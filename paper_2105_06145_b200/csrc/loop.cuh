@@ -1440,7 +1440,20 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     if (gtid == 0) ctrl->rounds = r - 1;
     // S6 output: strip the flag bit (every reached vertex was extracted; INF stays INF)
     if (p.nofo) {  // compacted ids: out[v] = delta[nofo[v]] for every caller id v
-        for (int64_t v = gtid; v < p.n_out; v += gsize) {
+        // 4 consecutive ids per thread per step (one 16-byte map load, 4 key loads in
+        // flight); nofo is a 256-byte-aligned workspace array
+        const int64_t n4 = p.n_out & ~3ll;
+        for (int64_t v = gtid * 4; v < n4; v += gsize * 4) {
+            const int4 u4 = __ldcg((const int4*)(p.nofo + v));
+            const int32_t u[4] = {u4.x, u4.y, u4.z, u4.w};
+            uint64_t x[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+                x[k] = (u[k] < p.n || u[k] == src) ? __ldcg((const unsigned long long*)(p.dist + u[k])) : kInf;
+#pragma unroll
+            for (int k = 0; k < 4; k++) p.out[v + k] = (x[k] != kInf && (x[k] & kTop)) ? (x[k] & kVal) : x[k];
+        }
+        for (int64_t v = n4 + gtid; v < p.n_out; v += gsize) {
             const int32_t u = p.nofo[v];
             const uint64_t x = (u < p.n || u == src) ? __ldcg((const unsigned long long*)(p.dist + u)) : kInf;
             p.out[v] = (x != kInf && (x & kTop)) ? (x & kVal) : x;
