@@ -332,7 +332,9 @@ def test_isolated_vertex_compaction(cuda_device):
     assert h_on.workspace.numel() > h_off.workspace.numel()
     for s in [int(g.source), int(nz[len(nz) // 2]), int(nz[-1]), int(iso[0]), int(iso[-1])]:
         want = oracle.dijkstra(g, source=s)
-        for pol, par, kw in (("rho", 256, {}), ("delta", 1 << 14, {}), ("bellman_ford", 0, dict(snapshot=True))):
+        for pol, par, kw in (("rho", 256, {}), ("delta", 1 << 14, {}), ("bellman_ford", 0, dict(snapshot=True)),
+                             ("rho", 64, dict(bidir=True)), ("dijkstra", 0, {}), ("delta_stepping", 1 << 12, {}),
+                             ("rho", 32, dict(exact=True, snapshot=True, nearfar=False))):
             d_on, st_on, _, e_on = h_on.run(s, pol, par, ext_counts=True, stats=True, **kw)
             d_off, st_off, _, e_off = h_off.run(s, pol, par, ext_counts=True, stats=True, **kw)
             _assert_same(P.dist_to_u64(d_on), want, f"compaction on s={s} {pol}")
