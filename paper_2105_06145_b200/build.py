@@ -51,7 +51,8 @@ def units(unit_defines=None):
 
 def deps():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
-                  glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(HERE, "..", "include", "sssp.h")]
+                  glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(HERE, "..", "include", "sssp.h"),
+                                                           os.path.abspath(__file__)]  # UNIT_DEFINES live here
 
 
 def up_to_date(out: str = OUT) -> bool:

@@ -85,6 +85,9 @@ constexpr int kWarps = kBlock / 32;
 #ifndef SSSP_SEG_HINT
 #define SSSP_SEG_HINT 1  // phase B: find a descriptor's segment by a forward scan from the last one
 #endif
+#ifndef SSSP_DEFER
+#define SSSP_DEFER 1  // kernels without fusion: batch the improving WriteMins, 32 CAS per round trip
+#endif
 #ifndef SSSP_NEAR_K
 #define SSSP_NEAR_K 8
 #endif
@@ -313,10 +316,16 @@ __device__ __forceinline__ int seg_of(const int64_t* pref, int64_t i) {
 }
 
 // --------------------------------------------------------------------- per-warp staging
+constexpr int kPend = 64;  // SSSP_DEFER: pending WriteMins per warp (drained at 32)
 struct WarpStage {
     int32_t take[kTBuf];  // ids that pass the theta test, extracted 32 at a time
     int32_t q[kQBuf];     // ids appended to the next queue
     uint64_t mins[32];    // bidirectional relaxation: per-vertex pulled minimum
+#if SSSP_DEFER
+    uint64_t pc[kPend];   // pending WriteMins: candidate ...
+    uint64_t pw[kPend];   // ... the word the filter read ...
+    int32_t pv[kPend];    // ... and the target
+#endif
 };
 struct FuseStage {        // FUSE kernels only (kept out of the others' shared memory, which is L1)
     uint64_t fd[kFBuf];   // fused vertices: key ...
@@ -349,6 +358,7 @@ struct Warp {  // per-warp working state (qn is warp-uniform)
     int32_t qn;
     int32_t fn;       // staged fused vertices (warp-uniform)
     int32_t fbudget;  // fusions left this round (warp-uniform)
+    int32_t pn;       // SSSP_DEFER: pending WriteMins (warp-uniform)
     Acc acc;
 #if SSSP_PROF
     // cycles in scan, take, light relax, queue flush, fuse_drain; fuse_drain batches;
@@ -461,6 +471,30 @@ __device__ __forceinline__ int write_min(uint64_t* dist, int32_t v, uint64_t c, 
     return kNone;
 }
 
+// SSSP_DEFER: run the `cnt` newest pending WriteMins, one per lane (one CAS round trip
+// for up to 32 of them), and stage the inserted ids.
+template <int POL, bool STATS, bool FUSE, bool BIDIR>
+__device__ __forceinline__ void run_pending(const RunParams& p, Warp& W, int32_t cnt) {
+#if SSSP_DEFER
+    const int lane = lane_id();
+    __syncwarp();
+    int out = kNone;
+    int32_t v = -1;
+    if (lane < cnt) {
+        const int32_t j = W.pn - cnt + lane;
+        v = W.st->pv[j];
+        out = write_min<POL, STATS, FUSE, BIDIR>(p.dist, v, W.st->pc[j], W.st->pw[j], false, W);
+    }
+    __syncwarp();
+    W.pn -= cnt;
+    wq_push1(W, out == kAppend, v);
+#endif
+}
+template <int POL, bool STATS, bool FUSE, bool BIDIR>
+__device__ __forceinline__ void drain_pending(const RunParams& p, Warp& W) {
+    while (SSSP_DEFER && !FUSE && !BIDIR && W.pn > 0) run_pending<POL, STATS, FUSE, BIDIR>(p, W, W.pn < 32 ? W.pn : 32);
+}
+
 // Relax kArcs arcs per lane (v < 0 = empty slot): filter loads, WriteMins, stage the
 // inserted ids (Alg. 1 lines 5-6).
 struct NoPull {
@@ -480,6 +514,30 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
 #pragma unroll
     for (int t = 0; t < kArcs; t++) cur[t] = v[t] >= 0 ? dist_filter_ld(p.dist + v[t]) : 0ull;
     pull(v, cur, c);  // bidirectional relaxation may lower the candidates (SURVEY f-2)
+    if (SSSP_DEFER && !FUSE && !BIDIR) {
+        // Deferred WriteMins: the improving candidates (a few per step in bulk rounds) are
+        // staged and their CAS issued 32 at a time, so a step waits on its key gathers only,
+        // not also on a CAS round trip.  Any order of WriteMins is valid, and the CAS
+        // re-checks the word it expects (a change in between just retries).
+#if SSSP_DEFER
+#pragma unroll
+        for (int t = 0; t < kArcs; t++) {
+            const bool imp = v[t] >= 0 && (cur[t] & kVal) > c[t];
+            const uint32_t m = __ballot_sync(kFull, imp);
+            if (!m) continue;
+            if (imp) {
+                const int32_t j = W.pn + __popc(m & lanemask_lt());
+                W.st->pv[j] = v[t];
+                W.st->pc[j] = c[t];
+                W.st->pw[j] = cur[t];
+            }
+            W.pn += __popc(m);
+            if (W.pn >= 32) run_pending<POL, STATS, FUSE, BIDIR>(p, W, 32);
+        }
+#endif
+        PROF_ADD(W, 7, trs);
+        return;
+    }
     // first CAS attempt of every slot issued back to back (one round trip, not kArcs),
     // then the rare retries
     uint64_t old[kArcs];
@@ -955,6 +1013,7 @@ __device__ __forceinline__ void phase_b(const RunParams& p, const Sharded<Desc>&
 
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __device__ __forceinline__ void flush_acc(const RunParams& p, int64_t r, Warp& W) {
+    drain_pending<POL, STATS, FUSE, BIDIR>(p, W);  // deferred WriteMins before the phase ends
     wq_flush(W);
     const int64_t dq = warp_sum(W.qdelta);
     if (lane_id() == 0 && dq) atomicAdd((unsigned long long*)(p.cta_delta + (r % 3) * kMaxCtas + blockIdx.x),
@@ -1105,6 +1164,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     W.shard = (int)(warp_rank() % kShards);
     W.qn = 0;
     W.fn = 0;
+    W.pn = 0;
     if (threadIdx.x == 0) tile_ctr[0] = tile_ctr[1] = 0;
     W.qdelta = 0;
     W.front = 0;
@@ -1392,6 +1452,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             phase_b<POL, STATS, FUSE, BIDIR>(p, CL, cpref, nl, W);
             if (STATS && lane_id() == 0) atomicAdd(&C->busy_b, (unsigned long long)(globaltimer() - tb));
         }
+        drain_pending<POL, STATS, FUSE, BIDIR>(p, W);  // deferred WriteMins count in min_Q
         if (uses_min(POL)) {
             if (phase_b_work) publish_min();  // now including phase B's WriteMins
             W.acc.minsucc = kInf;
