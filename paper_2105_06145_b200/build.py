@@ -24,12 +24,16 @@ POLICIES = 5  # SSSP_RHO .. SSSP_DELTA_STEPPING (include/sssp.h)
 
 
 # Unit-specific tuning constants (the constants of csrc/loop.cuh are compile-time): the
-# rho kernels without fusion relax 6 arcs per lane per step (more gathers in flight; the
-# fusion kernels spill with it).  A/B on rmat24: rho = 2^18 -2.6 %, 2^21 -6 %.
+# rho kernels without fusion relax more arcs per lane per step (more gathers in flight; the
+# fusion kernels spill with it).  Before deferred WriteMins, 6 arcs: rmat24 rho = 2^18
+# -2.6 %, 2^21 -6 % against 4.
 # The segment hint in phase B (forward scan instead of a binary search per descriptor)
 # helps BF / Delta* by ~2 % and costs the 6-arc rho unit ~2 % (register allocation), so
 # that unit keeps the binary search.
-UNIT_DEFINES = {(0, 0, 0): ["-DSSSP_ARCS=6", "-DSSSP_SEG_HINT=0"]}
+# With deferred WriteMins the rho unit does best at 5 arcs per lane (A/B against 6:
+# rmat24 rho = 2^18 -2.9 %, 2^17 -3.1 %, rmat20 -4 %; 7 arcs: +2 %).
+# The Delta* unit likewise (rmat24 -1.6 %, rmat20 -2.4 %); BF stays at 4 (+8-12 % with 5).
+UNIT_DEFINES = {(0, 0, 0): ["-DSSSP_ARCS=5", "-DSSSP_SEG_HINT=0"], (1, 0, 0): ["-DSSSP_ARCS=5"]}
 
 
 def units(unit_defines=None):
