@@ -168,8 +168,14 @@ class SSSP:
         With stats=True returns (dist, stats_dict, trace ndarray | None, ext_count tensor | None)."""
         torch = _torch()
         pol = POLICIES[policy] if isinstance(policy, str) else int(policy)
+        dev = self.offsets.device
         if out is None:
-            out = torch.empty(self.n, dtype=torch.int64, device=self.offsets.device)
+            out = torch.empty(self.n, dtype=torch.int64, device=dev)
+        # the kernel writes n uint64 words through the raw pointer: refuse anything smaller
+        if not (out.device == dev and out.dtype in (torch.int64, torch.uint64) and out.is_contiguous()
+                and out.numel() >= self.n):
+            raise ValueError(f"out must be a contiguous int64/uint64 tensor of >= {self.n} elements on {dev} "
+                             f"(got {tuple(out.shape)} {out.dtype} on {out.device})")
         o = sssp_run_opts()
         o.flags = (SSSP_RUN_RHO_EXACT if exact else 0) | (0 if warmup else SSSP_RUN_NO_WARMUP) | \
                   (SSSP_RUN_STATS if (stats or trace_cap) else 0) | (SSSP_RUN_SNAPSHOT if snapshot else 0) | \
@@ -179,14 +185,15 @@ class SSSP:
         o.seed = seed
         o.max_rounds = max_rounds
         trace = None
-        if trace_cap:
-            trace = torch.zeros(trace_cap * ROUND_WORDS, dtype=torch.int64, device=out.device)
-            o.d_trace = trace.data_ptr()
-            o.trace_cap = trace_cap
         ext = None
-        if ext_counts:
-            ext = torch.zeros(self.n, dtype=torch.int32, device=out.device)
-            o.d_ext_count = ext.data_ptr()
+        with torch.cuda.stream(self.stream):  # the fills are ordered before the launch on the same stream
+            if trace_cap:
+                trace = torch.zeros(trace_cap * ROUND_WORDS, dtype=torch.int64, device=dev)
+                o.d_trace = trace.data_ptr()
+                o.trace_cap = trace_cap
+            if ext_counts:
+                ext = torch.zeros(self.n, dtype=torch.int32, device=dev)
+                o.d_ext_count = ext.data_ptr()
         st = sssp_run_stats()
         with torch.cuda.stream(self.stream):
             _check(sssp_run_ex(self._h, int(source), pol, int(param), ctypes.byref(o), _ptr(out), ctypes.byref(st)),

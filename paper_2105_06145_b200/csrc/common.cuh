@@ -136,7 +136,8 @@ __device__ __forceinline__ int32_t warp_excl_scan_small(int32_t v, int32_t& tota
 // Requires a cooperative launch.  cooperative_groups' grid sync measured 1.2 us at
 // 296-444 CTAs on B200 vs 1.5-1.9 us for a hand-written arrive/spin counter
 // (scripts/bench_barrier.cu, profiles/bench_barrier_r1.log).
-__device__ __forceinline__ void grid_sync(unsigned* /*unused*/) { cooperative_groups::this_grid().sync(); }
+// (no counter argument: the hand-written arrive/spin barrier was replaced by this one)
+__device__ __forceinline__ void grid_sync() { cooperative_groups::this_grid().sync(); }
 
 // ------------------------------------------------------------------ sampling (reading R5/R6)
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {

@@ -76,47 +76,28 @@ constexpr int kWarps = kBlock / 32;
 #ifndef SSSP_PROF
 #define SSSP_PROF 0  // 1: STATS kernels also split phase-A warp time into parts (clock64)
 #endif
-#ifndef SSSP_DYN
-#define SSSP_DYN 1
-#endif
-#ifndef SSSP_LANE_LOCAL
-#define SSSP_LANE_LOCAL 1  // relax batches whose degrees are all <= kArcs lane-locally
-#endif
 #ifndef SSSP_SEG_HINT
 #define SSSP_SEG_HINT 1  // phase B: find a descriptor's segment by a forward scan from the last one
-#endif
-#ifndef SSSP_DEFER
-#define SSSP_DEFER 1  // kernels without fusion: batch the improving WriteMins, 32 CAS per round trip
-#endif
+#endif                   // (0: binary search; the rho unit without fusion uses 0, build.py)
 #ifndef SSSP_NEAR_K
 #define SSSP_NEAR_K 8
-#endif
-#ifndef SSSP_L1DIST
-#define SSSP_L1DIST 1
 #endif
 #ifndef SSSP_FUSE
 #define SSSP_FUSE 64
 #endif
-#ifndef SSSP_ENT
-#define SSSP_ENT 2
-#endif
-constexpr int kEnt = SSSP_ENT;               // queue entries per lane per Extract step (large queues)
+constexpr int kEnt = 2;                      // queue entries per lane per Extract step (large queues)
 constexpr int kQBuf = 256;                   // staged queue ids per warp (>= 32 * kArcs)
 constexpr int kTBuf = 32 * kEnt + 32;        // staged extracted ids per warp
 constexpr int kFBuf = 32 * kArcs + 64;       // fused vertices waiting for their relax, per warp
 constexpr int kFuseBudget = SSSP_FUSE;       // fused vertices per warp per round (0 = off)
 constexpr int kFuseMaxDeg = 1024;            // a fused vertex of higher degree goes back to Q
-#ifndef SSSP_CONTIG
-#define SSSP_CONTIG 16
-#endif
-constexpr int kContigTiles = SSSP_CONTIG;    // queue < kContigTiles*32 ids per warp: contiguous shares
+constexpr int kContigTiles = 16;             // queue < kContigTiles*32 ids per warp: contiguous shares
 constexpr int kSparseDeg = 20;               // fusion in rounds whose frontier averages < 20 arcs
 constexpr int kShards = 32;                  // append-list segments (+1 spill)
 constexpr int kSeg = kShards + 1;
 constexpr int kCntStride = 256;              // int32 words between counters (1 KB: distinct L2 slices)
 constexpr int kMaxCtas = 4096;
 constexpr int kPolicies = 5;
-constexpr bool kDyn = SSSP_DYN;               // phase A: tiles dealt to CTAs, taken by warps dynamically
 constexpr int kProf = 8;                     // SSSP_PROF counters per round
 constexpr int kNearK = SSSP_NEAR_K;          // near queue target: ~kNearK rounds of extraction
 #ifndef SSSP_FAR_SAMPLES
@@ -199,7 +180,6 @@ struct RunParams {
     int32_t* counters;  // [3 slots][2 lists: queue, chunks][kSeg] * kCntStride
     uint64_t* cta_min;  // [3 slots][kMaxCtas]: per-CTA min for Delta / Dijkstra
     int64_t* cta_delta; // [3 slots][kMaxCtas]: per-CTA change of |Q| (inserts - extractions)
-    int64_t* cta_front; // [3 slots][kMaxCtas]: per-CTA (arcs << 32 | vertices) extracted
     Desc* light;
     uint64_t* samples;
     Ctrl* ctrl;
@@ -272,8 +252,7 @@ __device__ __forceinline__ int64_t warp_rank() { return (int64_t)(threadIdx.x >>
 // decreases, and every grid barrier's fence invalidates L1), so it can only cause a CAS
 // that then fails and retries with the word the CAS returned: never a lost update.
 __device__ __forceinline__ uint64_t dist_filter_ld(const uint64_t* p) {
-    if (SSSP_L1DIST) return __ldca((const unsigned long long*)p);
-    return ld_cg_u64(p);
+    return __ldca((const unsigned long long*)p);
 }
 
 __host__ __device__ constexpr bool uses_min(int pol) {
@@ -316,16 +295,14 @@ __device__ __forceinline__ int seg_of(const int64_t* pref, int64_t i) {
 }
 
 // --------------------------------------------------------------------- per-warp staging
-constexpr int kPend = 64;  // SSSP_DEFER: pending WriteMins per warp (drained at 32)
+constexpr int kPend = 64;  // deferred WriteMins: pending WriteMins per warp (drained at 32)
 struct WarpStage {
     int32_t take[kTBuf];  // ids that pass the theta test, extracted 32 at a time
     int32_t q[kQBuf];     // ids appended to the next queue
     uint64_t mins[32];    // bidirectional relaxation: per-vertex pulled minimum
-#if SSSP_DEFER
-    uint64_t pc[kPend];   // pending WriteMins: candidate ...
+    uint64_t pc[kPend];   // deferred WriteMins (kernels without fusion): candidate ...
     uint64_t pw[kPend];   // ... the word the filter read ...
     int32_t pv[kPend];    // ... and the target
-#endif
 };
 struct FuseStage {        // FUSE kernels only (kept out of the others' shared memory, which is L1)
     uint64_t fd[kFBuf];   // fused vertices: key ...
@@ -353,12 +330,11 @@ struct Warp {  // per-warp working state (qn is warp-uniform)
     uint64_t fuse_theta;  // live rounds: theta (a vertex outside Q improved to <= theta is
                           // extracted on the spot, DESIGN.md §5 "fusion"); 0 = no fusion
     int64_t qdelta;       // this lane's inserts - extractions (|Q| bookkeeping)
-    uint64_t front;       // this lane's extractions: (arcs << 32) | vertices
     int shard;
     int32_t qn;
     int32_t fn;       // staged fused vertices (warp-uniform)
     int32_t fbudget;  // fusions left this round (warp-uniform)
-    int32_t pn;       // SSSP_DEFER: pending WriteMins (warp-uniform)
+    int32_t pn;       // deferred WriteMins: pending WriteMins (warp-uniform)
     Acc acc;
 #if SSSP_PROF
     // cycles in scan, take, light relax, queue flush, fuse_drain; fuse_drain batches;
@@ -471,11 +447,10 @@ __device__ __forceinline__ int write_min(uint64_t* dist, int32_t v, uint64_t c, 
     return kNone;
 }
 
-// SSSP_DEFER: run the `cnt` newest pending WriteMins, one per lane (one CAS round trip
+// Deferred WriteMins: run the `cnt` newest pending ones, one per lane (one CAS round trip
 // for up to 32 of them), and stage the inserted ids.
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __device__ __forceinline__ void run_pending(const RunParams& p, Warp& W, int32_t cnt) {
-#if SSSP_DEFER
     const int lane = lane_id();
     __syncwarp();
     int out = kNone;
@@ -488,11 +463,10 @@ __device__ __forceinline__ void run_pending(const RunParams& p, Warp& W, int32_t
     __syncwarp();
     W.pn -= cnt;
     wq_push1(W, out == kAppend, v);
-#endif
 }
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __device__ __forceinline__ void drain_pending(const RunParams& p, Warp& W) {
-    while (SSSP_DEFER && !FUSE && !BIDIR && W.pn > 0) run_pending<POL, STATS, FUSE, BIDIR>(p, W, W.pn < 32 ? W.pn : 32);
+    while (!FUSE && !BIDIR && W.pn > 0) run_pending<POL, STATS, FUSE, BIDIR>(p, W, W.pn < 32 ? W.pn : 32);
 }
 
 // Relax kArcs arcs per lane (v < 0 = empty slot): filter loads, WriteMins, stage the
@@ -514,12 +488,11 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
 #pragma unroll
     for (int t = 0; t < kArcs; t++) cur[t] = v[t] >= 0 ? dist_filter_ld(p.dist + v[t]) : 0ull;
     pull(v, cur, c);  // bidirectional relaxation may lower the candidates (SURVEY f-2)
-    if (SSSP_DEFER && !FUSE && !BIDIR) {
+    if constexpr (!FUSE && !BIDIR) {
         // Deferred WriteMins: the improving candidates (a few per step in bulk rounds) are
         // staged and their CAS issued 32 at a time, so a step waits on its key gathers only,
         // not also on a CAS round trip.  Any order of WriteMins is valid, and the CAS
         // re-checks the word it expects (a change in between just retries).
-#if SSSP_DEFER
 #pragma unroll
         for (int t = 0; t < kArcs; t++) {
             const bool imp = v[t] >= 0 && (cur[t] & kVal) > c[t];
@@ -534,10 +507,9 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
             W.pn += __popc(m);
             if (W.pn >= 32) run_pending<POL, STATS, FUSE, BIDIR>(p, W, 32);
         }
-#endif
         PROF_ADD(W, 7, trs);
         return;
-    }
+    } else {
     // first CAS attempt of every slot issued back to back (one round trip, not kArcs),
     // then the rare retries
     uint64_t old[kArcs];
@@ -594,6 +566,7 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
         W.fbudget -= tot;
     }
     PROF_ADD(W, 7, trs);
+    }
 }
 
 // One chunk: arcs [beg, beg+len) of a vertex with key d, len <= kChunk.  Lane-strided
@@ -663,7 +636,7 @@ template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, int32_t beg, int32_t deg, Warp& W,
                                                int32_t uid = -1) {
     const int lane = lane_id();
-    if (SSSP_LANE_LOCAL && __all_sync(kFull, deg <= kArcs)) {
+    if (__all_sync(kFull, deg <= kArcs)) {
         // every vertex fits one lane: lane-local arcs, no scan or owner search (fusion
         // chains on grids are latency chains: A/B grid4096 Delta* 63.2 -> 59.0 ms, grid256
         // -4 %, rgg4m +1.5-2.7 %, rmat20/24 within 1 %)
@@ -766,7 +739,6 @@ __device__ __forceinline__ void fuse_drain(const RunParams& p, Warp& W) {
         wq_push1(W, back, hub);
         if (id >= 0) {
             if (p.ext_count) atomicAdd(p.ext_count + (p.ofno ? p.ofno[id] : id), 1);
-            W.front += 1 | ((uint64_t)deg << 32);
             if (STATS) {
                 W.acc.fused++;  // counted as inserted and extracted (the |Q| identity holds)
                 W.acc.inserts++;
@@ -841,8 +813,6 @@ __device__ __forceinline__ void take_batch(const RunParams& p, int32_t cnt, cons
     id = ok ? id : -1;
     if (id >= 0) {
         W.qdelta--;
-        W.front += 1;
-        W.front += (uint64_t)deg << 32;
         if (p.ext_count) atomicAdd(p.ext_count + (p.ofno ? p.ofno[id] : id), 1);
     }
     if (STATS && id >= 0) {
@@ -886,14 +856,14 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
     const int64_t lo = contig ? gw * q / nwarps : gw * (32 * ent);
     const int64_t hi = contig ? (gw + 1) * q / nwarps : q;
     const int64_t stride = contig ? 32 * ent : nwarps * (32 * ent);
-    // SSSP_DYN (kernels without fusion, queues of >= one 32-id tile per warp): the queue
+    // Dynamic tiles (kernels without fusion, queues of >= one 32-id tile per warp): the queue
     // is cut into 32*ent-id tiles dealt to the CTAs round-robin (CTA c owns tiles c,
     // c + grid, ...: correlated neighbours land on different SMs), and each CTA's warps
     // take its tiles from a shared-memory counter (no warp idles while its CTA has work).
     // With fusion, every warp keeps its own thin share: there each warp seeds its own
     // local search (dynamic tiles left most warps idle and took grid4096 from 932 to
     // 4,422 rounds).
-    const bool dyn = kDyn && !FUSE && q >= 32 * nwarps;
+    const bool dyn = !FUSE && q >= 32 * nwarps;
     for (int64_t it = 0;; it++) {
         int64_t base, lim;
         if (dyn) {
@@ -1019,10 +989,6 @@ __device__ __forceinline__ void flush_acc(const RunParams& p, int64_t r, Warp& W
     if (lane_id() == 0 && dq) atomicAdd((unsigned long long*)(p.cta_delta + (r % 3) * kMaxCtas + blockIdx.x),
                                         (unsigned long long)dq);
     W.qdelta = 0;
-    const uint64_t fr = warp_sum(W.front);
-    if (lane_id() == 0 && fr) atomicAdd((unsigned long long*)(p.cta_front + (r % 3) * kMaxCtas + blockIdx.x),
-                                        (unsigned long long)fr);
-    W.front = 0;
     if (STATS) {
         const uint32_t s = warp_sum(W.acc.succ), ins = warp_sum(W.acc.inserts), fu = warp_sum(W.acc.fused);
         const uint64_t fe = warp_sum(W.acc.fused_edges);
@@ -1153,7 +1119,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     __shared__ int64_t cpref[kSeg + 1];  // segment prefix of the round's chunk list
     __shared__ uint64_t bc_u[3];         // min_Q (Delta / Dijkstra), CTA-0 theta, CTA-0 split
     __shared__ int64_t bc_dq;
-    __shared__ uint64_t bc_front;
     __shared__ int32_t bc_nl, bc_cnt;
     __shared__ int32_t tile_ctr[2];      // phase-A tile counters, by round parity
     __shared__ uint64_t red[kWarps];
@@ -1167,7 +1132,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     W.pn = 0;
     if (threadIdx.x == 0) tile_ctr[0] = tile_ctr[1] = 0;
     W.qdelta = 0;
-    W.front = 0;
 #if SSSP_PROF
     for (int i = 0; i < kProf; i++) W.prof[i] = 0;
 #endif
@@ -1186,7 +1150,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     for (int64_t i = gtid; i < 3 * kMaxCtas; i += gsize) {
         p.cta_min[i] = kInf;
         p.cta_delta[i] = 0;
-        p.cta_front[i] = 0;
     }
     if (gtid == 0) {
         p.qbuf[1][0] = src;  // Q_1 lives in qbuf[1], shard 0
@@ -1197,12 +1160,12 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         ctrl->tot_qscan = ctrl->max_q = ctrl->max_f = 0;
         ctrl->tot_dense = 0;
     }
-    grid_sync(nullptr);
+    grid_sync();
     if (gtid == 0) {
         p.counters[0] = 1;  // |Q_1| = 1 (slot 0, queue list, shard 0)
         p.cta_min[0] = 0;   // min_Q delta = delta[s] = 0
     }
-    grid_sync(nullptr);
+    grid_sync();
 
     // near/far queue for rho only (Delta* / BF / Dijkstra keep split = +inf: all of Q listed)
     const bool nearfar = POL == SSSP_RHO && !(p.flags & SSSP_RUN_NO_NEARFAR);
@@ -1216,16 +1179,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         const Sharded<int32_t> QC = queue_of(p, r);
         const Sharded<Desc> CL = chunks_of(p, r);
         // |Q_r| = |Q_{r-1}| + sum over CTAs of (inserts - extractions) in round r-1
-        // warps 1-3, in parallel with warp 0's load_prefix: the previous round's |Q| delta,
-        // frontier size and arcs, and min_Q delta (Delta* / Dijkstra)
-        if ((threadIdx.x >> 5) == 2 && r > 1) {
-            const int lane = lane_id();
-            const int64_t* cf = p.cta_front + ((r + 2) % 3) * kMaxCtas;
-            uint64_t sf = 0;
-            for (int i = lane; i < (int)gridDim.x; i += 32) sf += __ldcg((const unsigned long long*)(cf + i));
-            sf = warp_sum(sf);
-            if (lane == 0) bc_front = sf;
-        }
+        // warps 1 and 3, in parallel with warp 0's load_prefix: the previous round's |Q|
+        // delta and min_Q delta (Delta* / Dijkstra)
         if ((threadIdx.x >> 5) == 1 && r > 1) {
             const int lane = lane_id();
             const int64_t* cd = p.cta_delta + ((r + 2) % 3) * kMaxCtas;
@@ -1265,7 +1220,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         }
         if (threadIdx.x == 0) {
             p.cta_delta[((r + 1) % 3) * kMaxCtas + blockIdx.x] = 0;
-            p.cta_front[((r + 1) % 3) * kMaxCtas + blockIdx.x] = 0;
         }
         W.qnext = queue_of(p, r + 1);
         W.C = C;
@@ -1326,14 +1280,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                                                                             s_keys, sm, &bc_cnt);
                         if (threadIdx.x == 0) C->split = h;
                     }
-                    grid_sync(nullptr);
+                    grid_sync();
                     if (threadIdx.x == 0) bc_u[2] = __ldcg((const unsigned long long*)&C->split);
                     __syncthreads();
                     hi = bc_u[2];
                 }
                 far_to_near(p, QC, split, hi, W);
                 dense += p.n;
-                grid_sync(nullptr);
+                grid_sync();
                 load_prefix(QC, qpref);
                 qn = qpref[kSeg];
                 split = hi;
@@ -1354,7 +1308,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                     const uint64_t h = cta_kth_smallest(SmemKey{s_keys}, (int64_t)s2, k, sm);
                     if (threadIdx.x == 0) C->split = h;
                 }
-                grid_sync(nullptr);
+                grid_sync();
                 if (threadIdx.x == 0) bc_u[2] = __ldcg((const unsigned long long*)&C->split);
                 __syncthreads();
                 if (bc_u[2] < split) {
@@ -1393,18 +1347,15 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
                     }
                     if (threadIdx.x == 0) C->theta = th;
                 }
-                grid_sync(nullptr);
+                grid_sync();
                 if (threadIdx.x == 0) bc_u[1] = __ldcg((const unsigned long long*)&C->theta);
                 __syncthreads();
                 theta = bc_u[1];
             }
         }
         W.split = split;
-        // fusion in live rounds that are sparse: a sparse graph, or a previous frontier that
-        // averaged fewer than 20 arcs per vertex (the paper's rule)
-        const uint64_t fv = r > 1 ? (bc_front & 0xFFFFFFFFull) : 1, fe = r > 1 ? (bc_front >> 32) : 0;
-        const bool sparse = p.m < (int64_t)kSparseDeg * p.n || fe < (uint64_t)kSparseDeg * fv;
-        W.fuse_theta = (snap || !sparse) ? 0 : theta;
+        // fusion in live rounds (FUSE kernels are launched for sparse graphs only, run.cu)
+        W.fuse_theta = (FUSE && !snap) ? theta : 0;
         W.fbudget = p.fuse_budget;
         if (STATS && gtid == 0) t1 = globaltimer();
 
@@ -1439,7 +1390,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             }
         };
         if (uses_min(POL)) publish_min();
-        grid_sync(nullptr);
+        grid_sync();
         if (STATS && gtid == 0) t2 = globaltimer();
         // ---- phase B: heavy chunks (+ light list in snapshot mode)
         load_prefix(CL, cpref);
@@ -1459,9 +1410,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         }
         if (phase_b_work) {
             flush_acc<POL, STATS, FUSE, BIDIR>(p, r, W);
-            grid_sync(nullptr);
+            grid_sync();
         } else if (STATS) {
-            grid_sync(nullptr);
+            grid_sync();
         }
         if (STATS && gtid == 0) t3 = globaltimer();
 

@@ -101,7 +101,6 @@ struct Layout {
     int32_t* counters;
     uint64_t* cta_min;
     int64_t* cta_delta;
-    int64_t* cta_front;
     Desc* light;
     uint64_t* samples;
     Ctrl* ctrl;
@@ -137,7 +136,6 @@ Layout carve(void* base, int32_t n, int64_t m, uint32_t flags) {
     L.counters = c.take<int32_t>((size_t)3 * 2 * kSeg * kCntStride);
     L.cta_min = c.take<uint64_t>((size_t)3 * kMaxCtas);
     L.cta_delta = c.take<int64_t>((size_t)3 * kMaxCtas);
-    L.cta_front = c.take<int64_t>((size_t)3 * kMaxCtas);
     L.dist = c.take<uint64_t>(n);
     L.dist2 = c.take<uint64_t>(n);
     L.q0 = c.take<int32_t>(qlen);
@@ -187,12 +185,14 @@ sssp_status launch_run(sssp_handle* h, int32_t source, sssp_policy policy, uint6
     cudaError_t de = cudaSetDevice(h->device);
     if (de != cudaSuccess) return cuda_error(de, "cudaSetDevice");
     const bool st = (o.flags & SSSP_RUN_STATS) != 0;
-    // fusion ("local relaxation within theta") in live rounds of sparse graphs:
-    // the paper applies it when the average degree is below 20
-    // (measured: fusing the low-degree late rounds of R-MAT re-relaxes 17% more arcs and
-    // costs 50% time, so dense graphs do not fuse at all; see DESIGN.md fusion)
-    const bool fu = !(o.flags & (SSSP_RUN_SNAPSHOT | SSSP_RUN_NO_FUSE)) && policy != SSSP_DIJKSTRA &&
-                    h->m < (int64_t)kSparseDeg * h->n;
+    // fusion ("local relaxation within theta"): the paper applies it in its
+    // Delta*- and rho-stepping in sparse rounds, average degree below 20
+    // (P:1387-1388).  Here the degree rule is per graph (m < 20 n): fusing the low-degree
+    // late rounds of R-MAT re-relaxed 17 % more arcs and cost 50 % time (DESIGN.md fusion).
+    // Bellman-Ford, Delta-stepping with FinishCheck and Dijkstra never fuse, so their
+    // rounds and counters describe those algorithms.
+    const bool fu = !(o.flags & (SSSP_RUN_SNAPSHOT | SSSP_RUN_NO_FUSE)) &&
+                    (policy == SSSP_RHO || policy == SSSP_DELTA) && h->m < (int64_t)kSparseDeg * h->n;
     RunParams p = h->base;
     if (p.nofo) {  // compacted ids: delta lives in the workspace, the output pass maps it back
         p.dist = h->dint;
@@ -338,7 +338,6 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
     b.counters = L.counters;
     b.cta_min = L.cta_min;
     b.cta_delta = L.cta_delta;
-    b.cta_front = L.cta_front;
     b.light = L.light;
     b.samples = L.samples;
     b.ctrl = L.ctrl;
@@ -353,7 +352,7 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
                     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kernel_for(pol, st, sn),
                                                                       kBlock, smem);
                 if (e != cudaSuccess || per_sm < 1) {
-                    delete h;
+                    sssp_destroy(h);
                     return e != cudaSuccess ? cuda_error(e, "occupancy query")
                                             : set_error(SSSP_ERR_DEVICE, "round-loop kernel cannot be resident");
                 }
@@ -368,10 +367,10 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
     }
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
-        delete h;
+        sssp_destroy(h);  // every member is value-initialised; destroy null-checks each
         return cuda_error(e, "sssp_create: host resources");
     }
-    // the barrier counter must start at a multiple of 2^31; the rest is reset per run
+    // control block zeroed once (every run resets what it uses in its prologue)
     e = cudaMemsetAsync(L.ctrl, 0, sizeof(Ctrl), h->stream);
     if (e == cudaSuccess && (flags & SSSP_VALIDATE)) {
         cudaMemsetAsync(L.err, 0, sizeof(int32_t), h->stream);
@@ -381,8 +380,7 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
         if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, L.err, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
         if (e == cudaSuccess && herr) {
-            cudaFreeHost(h->h_ctrl);
-            delete h;
+            sssp_destroy(h);
             return set_error(SSSP_ERR_INVALID_GRAPH, "sssp_create: invalid CSR (%s%s%s%s)",
                              (herr & 1) ? "offsets[0]!=0 or offsets[n]!=m " : "", (herr & 2) ? "offsets decrease " : "",
                              (herr & 4) ? "index out of range " : "", (herr & 8) ? "weight < 1" : "");
@@ -396,8 +394,7 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
         e = cudaGetLastError();
     }
     if (e != cudaSuccess) {
-        cudaFreeHost(h->h_ctrl);
-        delete h;
+        sssp_destroy(h);
         return cuda_error(e, "sssp_create");
     }
     *out = h;
