@@ -48,7 +48,9 @@ def parse():
     ap.add_argument("--param", type=int, default=None)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-arc-budget", type=int, default=200_000_000)
+    ap.add_argument("--cpu-arc-budget", type=int, default=-1,
+                    help="cpu_baseline: stop the oracle after this many arc scans (-1: full run)")
+    ap.add_argument("--sources", type=int, default=10, help="secondary figure: seeded non-isolated sources")
     ap.add_argument("--no-flush", action="store_true")
     return ap.parse_args()
 
@@ -172,7 +174,8 @@ def emit(obj):
 
 # ----------------------------------------------------------------------------- CPU oracle arms
 def cpu_oracle_sample(g, source, arc_budget):
-    """Bounded sample of the oracle (plain binary-heap Dijkstra, 1 thread) on the same graph."""
+    """The oracle (plain binary-heap Dijkstra, 1 thread) on the same graph, stopped after
+    `arc_budget` arc scans (arc_budget >= m: the full run)."""
     import oracle
 
     t0 = time.perf_counter()
@@ -181,15 +184,27 @@ def cpu_oracle_sample(g, source, arc_budget):
     return scanned, settled, dt
 
 
+def seeded_sources(g, k, seed=2105):
+    """k seeded random non-isolated sources (the paper averages 10 sources)."""
+    import numpy as np
+
+    nz = np.flatnonzero(g.degrees > 0)
+    rs = np.random.default_rng(seed)
+    return [int(v) for v in rs.choice(nz, size=min(k, len(nz)), replace=False)]
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return  # rank 0 alone runs the CPU oracle arm
     g = make_graph(args.config)
     param = DEFAULT_PARAM[args.policy] if args.param is None else args.param
-    budget = min(g.m, 20_000_000)
+    # each timed step a bounded sample sized so that K steps scan ~10 m arcs in total (a full
+    # run per step for K <= 10; ~20 s per full run on rmat24): the whole arm ends in a few
+    # minutes.  Warm-up steps (untimed) are 1 % samples: they only warm the host caches.
+    budget = g.m if args.steps <= 10 else g.m * 10 // args.steps
     for _ in range(args.warmup):
-        cpu_oracle_sample(g, g.source, budget)
+        cpu_oracle_sample(g, g.source, max(1, g.m // 100))
     tot_arcs, tot_t, settled = 0, 0.0, 0
     for _ in range(args.steps):
         a, s, dt = cpu_oracle_sample(g, g.source, budget)
@@ -197,14 +212,16 @@ def run_reference(args):
         tot_t += dt
         settled = s
     gteps = tot_arcs / tot_t / 1e9
-    sample = (f"binary-heap Dijkstra (oracle/, 1 thread) from the workload source, stopped after {budget} arc "
-              f"scans ({settled} vertices settled) per step")
+    sample = (f"binary-heap Dijkstra (oracle/, 1 host thread of {os.cpu_count()}) from the workload source, "
+              + ("full run per step" if budget >= g.m else f"stopped after {budget} arc scans per step")
+              + f" ({settled} vertices settled); GTEPS = arcs scanned / time")
     emit({"impl": "reference", "metric": "SSSP GTEPS (m / device time per source)", "value": gteps,
           "unit": "GTEPS", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
           "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
           "vs_baseline": None, "dtype": "u64", "data": "synthetic",
           "config": workload_config(args, g, g.source, param, ws),
-          "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": 1, "kind": "oracle", "sample": sample},
+          "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": 1, "kind": "oracle", "sample": sample,
+                           "host_threads": os.cpu_count()},
           "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
 
@@ -280,12 +297,32 @@ def main():
     e2e_s = max_over_ranks(time.perf_counter() - t0, ws, dist, dev)
     e2e = ws * g.m * args.steps / e2e_s / 1e9
 
-    # algorithmic bytes from a counters run of the same workload
-    _, st, _, _ = h.run(source, args.policy, param, out=out, stats=True, seed=args.seed)
-    b_extract = 8 * st["queue_scanned"] + 8 * st["dense_scanned"]
-    b_relax = 8 * st["extracted"] + 16 * st["edges"]
-    b_touched = b_extract + b_relax
+    # algorithmic bytes: counters runs (the STATS variant
+    # of the kernel) with the SAME seeds as the timed steps, averaged, so that bytes and time
+    # describe the same rounds (sampled theta depends on the seed)
+    bts, sts = [], []
+    for k in range(args.steps):
+        _, st, _, _ = h.run(source, args.policy, param, out=out, stats=True, seed=args.seed + k)
+        bts.append(8 * st["queue_scanned"] + 8 * st["dense_scanned"] + 8 * st["extracted"] + 16 * st["edges"])
+        sts.append(st)
+    b_touched = statistics.mean(bts)
     kern_avg = statistics.mean(kern_ms)
+
+    # secondary figure: seeded non-isolated sources (the paper averages 10 sources)
+    multi = None
+    if args.sources > 0:
+        ms_src = []
+        for v in seeded_sources(g, args.sources):
+            h.run(v, args.policy, param, out=out, seed=args.seed)
+            if flush is not None:
+                flush.zero_()
+            h.run(v, args.policy, param, out=out, seed=args.seed)
+            ms_src.append(h.last_stats["kernel_ms"])
+        multi = {"sources": len(ms_src), "kernel_ms_mean": statistics.mean(ms_src),
+                 "kernel_ms_min": min(ms_src), "kernel_ms_max": max(ms_src),
+                 "gteps_mean": statistics.mean(g.m / t / 1e6 for t in ms_src),
+                 "note": "seeded random non-isolated sources (numpy default_rng(2105)), one warm run then one "
+                         "timed run each after an L2 flush; GTEPS = m / time"}
     peak, peak_src = load_peaks()
     achieved = b_touched / (kern_avg * 1e-3) / 1e9
     traffic, traffic_src = load_traffic(args.config, args.policy)
@@ -296,15 +333,21 @@ def main():
         return
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
-        budget = min(g.m, args.cpu_arc_budget)
+        budget = g.m if args.cpu_arc_budget < 0 else min(g.m, args.cpu_arc_budget)
         scanned, settled, dt = cpu_oracle_sample(g, source, budget)
-        cpu = {"value": scanned / dt / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
-               "sample": f"binary-heap Dijkstra (oracle/, 1 host thread of {os.cpu_count()}) from the same source, "
-                         f"stopped after {scanned} arc scans ({settled} vertices settled), {dt:.1f} s"}
+        full = budget >= g.m
+        cpu = {"value": (g.m if full else scanned) / dt / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+               "host_threads": os.cpu_count(), "seconds": dt,
+               "sample": (f"full binary-heap Dijkstra (oracle/, 1 host thread of {os.cpu_count()}) from the same "
+                          f"source: {settled} vertices settled, {scanned} arcs scanned, {dt:.1f} s; GTEPS = m / time"
+                          if full else
+                          f"binary-heap Dijkstra (oracle/, 1 host thread of {os.cpu_count()}) from the same source, "
+                          f"stopped after {scanned} arc scans ({settled} vertices settled), {dt:.1f} s")}
     emit({"metric": "SSSP GTEPS (m / device time per source)", "value": value, "unit": "GTEPS", "n_gpus": ws,
           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
           "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
           "config": workload_config(args, g, g.source, param, ws),
+          "multi_source": multi,
           "run": {"source_this_rank": source, "l2_flushed": flush is not None,
                   "rounds_median": statistics.median(rounds), "kernel_ms_mean": kern_avg,
                   "grid": [st["grid_blocks"], st["block_threads"]], "gen_s": round(t_gen, 1)},
@@ -313,7 +356,8 @@ def main():
                        "frac_of_8TBps": achieved / 8000.0,
                        "algorithmic_bytes_per_launch": b_touched,
                        "bytes_formula": "8*(ids scanned by Extract + vertices read by near/far dense passes) + 8*sum|F_r| "
-                                           "+ 16*sum E_r (SURVEY 8(d) B_touched; DESIGN.md §5)",
+                                           "+ 16*sum E_r (SURVEY 8(d) B_touched; DESIGN.md §5), mean over counters "
+                                           "runs with the timed steps' seeds",
                        "traffic_source": traffic_src},
           "cpu_baseline": cpu,
           "e2e": {"value": e2e, "unit": "GTEPS", "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 8 * g.n,
@@ -322,8 +366,9 @@ def main():
                           "of step i overlapping the run of step i+1; host wall clock"},
           "gpu_launches": args.steps,
           "clocks": clocks,
-          "counters": {k: st[k] for k in ("rounds", "extracted", "edges", "succ", "inserts", "queue_scanned",
-                                          "dense_scanned", "max_queue", "max_frontier")}})
+          "counters": {k: statistics.mean(x[k] for x in sts) for k in
+                       ("rounds", "extracted", "edges", "succ", "inserts", "queue_scanned", "dense_scanned",
+                        "max_queue", "max_frontier")}})
     if ws > 1:
         dist.destroy_process_group()
 

@@ -89,13 +89,16 @@ def dijkstra(g, source=None, with_hops=False):
     return (dist, hops) if with_hops else dist
 
 
-def dijkstra_budget(g, source, arc_budget):
-    """Dijkstra stopped after `arc_budget` arc scans; returns (arcs_scanned, settled)."""
+def dijkstra_budget(g, source, arc_budget, return_dist=False):
+    """Dijkstra stopped before the first pop once `arc_budget` arcs were scanned (the measurement
+    sample of bench.py); returns (arcs_scanned, settled) [, tentative distances]."""
     off, idx, w = _csr(g)
     dist = np.empty(g.n, np.uint64)
     settled = ctypes.c_int64(0)
     scanned = _load().oracle_dijkstra_budget(g.n, off.ctypes.data, idx.ctypes.data, w.ctypes.data, source,
                                              dist.ctypes.data, int(arc_budget), ctypes.addressof(settled))
+    if return_dist:
+        return int(scanned), int(settled.value), dist
     return int(scanned), int(settled.value)
 
 

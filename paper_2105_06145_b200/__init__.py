@@ -48,7 +48,7 @@ class SSSPError(RuntimeError):
 class sssp_run_opts(ctypes.Structure):
     _fields_ = [("flags", ctypes.c_uint32), ("fuse_budget", ctypes.c_uint32), ("seed", ctypes.c_uint64),
                 ("max_rounds", ctypes.c_int64), ("d_trace", ctypes.c_void_p), ("trace_cap", ctypes.c_int64),
-                ("d_ext_count", ctypes.c_void_p)]
+                ("d_ext_count", ctypes.c_void_p), ("fuse_depth", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 class sssp_run_stats(ctypes.Structure):
@@ -162,7 +162,7 @@ class SSSP:
 
     def run(self, source, policy="rho", param=0, out=None, stats=False, trace_cap=0, ext_counts=False,
             exact=False, warmup=True, seed=0, max_rounds=0, snapshot=False, nearfar=True, fuse=True,
-            fuse_budget=0, bidir=False):
+            fuse_budget=0, bidir=False, fuse_depth=0):
         """Alg. 1 from `source`; returns a uint64-valued int64 tensor of distances (INF = -1 as int64).
 
         With stats=True returns (dist, stats_dict, trace ndarray | None, ext_count tensor | None)."""
@@ -182,6 +182,7 @@ class SSSP:
                   (0 if nearfar else SSSP_RUN_NO_NEARFAR) | (0 if fuse else SSSP_RUN_NO_FUSE) | \
             (SSSP_RUN_BIDIR if bidir else 0)
         o.fuse_budget = fuse_budget
+        o.fuse_depth = fuse_depth
         o.seed = seed
         o.max_rounds = max_rounds
         trace = None

@@ -90,6 +90,10 @@ constexpr int kQBuf = 256;                   // staged queue ids per warp (>= 32
 constexpr int kTBuf = 32 * kEnt + 32;        // staged extracted ids per warp
 constexpr int kFBuf = 32 * kArcs + 64;       // fused vertices waiting for their relax, per warp
 constexpr int kFuseBudget = SSSP_FUSE;       // fused vertices per warp per round (0 = off)
+#ifndef SSSP_FUSE_DEPTH
+#define SSSP_FUSE_DEPTH 1000000
+#endif
+constexpr int kFuseDepth = SSSP_FUSE_DEPTH;  // hops a local search may go from its extracted seed
 constexpr int kFuseMaxDeg = 1024;            // a fused vertex of higher degree goes back to Q
 constexpr int kContigTiles = 16;             // queue < kContigTiles*32 ids per warp: contiguous shares
 constexpr int kSparseDeg = 20;               // fusion in rounds whose frontier averages < 20 arcs
@@ -191,6 +195,7 @@ struct RunParams {
     int64_t trace_cap;
     int32_t* ext_count;
     int32_t fuse_budget;  // fused vertices per warp per round (FUSE kernels)
+    int32_t fuse_depth;   // hops from the extracted seed a fused vertex may lie (FUSE kernels)
 };
 
 __device__ __forceinline__ int32_t* counters_of(const RunParams& p, int slot, int list) {
@@ -306,7 +311,8 @@ struct WarpStage {
 };
 struct FuseStage {        // FUSE kernels only (kept out of the others' shared memory, which is L1)
     uint64_t fd[kFBuf];   // fused vertices: key ...
-    int32_t fid[kFBuf];   // ... and id
+    int32_t fid[kFBuf];   // ... id ...
+    int32_t fdep[kFBuf];  // ... and hops from the extracted seed
 };
 
 // dynamic shared memory: per-warp stages, theta samples, select scratch [, fuse stages]
@@ -428,6 +434,8 @@ enum { kNone = 0, kAppend = 1, kFused = 2 };
 __device__ __forceinline__ bool fuses(bool fuse, uint64_t w, uint64_t c, const Warp& W) {
     return fuse && (w & kTop) && c <= W.fuse_theta;
 }
+// FUSE kernels: slot t of a relax step may fuse (its source vertex lies < fuse_depth hops from
+// its extracted seed) iff bit t of the step's mask is set
 
 // WriteMin(delta[v], c) on the packed word, given a prior read `w`: CAS retries.
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
@@ -477,7 +485,8 @@ struct NoPull {
 
 template <int POL, bool STATS, bool FUSE, bool BIDIR, typename Pull = NoPull>
 __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&v)[kArcs], uint64_t (&c)[kArcs],
-                                            Warp& W, Pull pull = Pull()) {
+                                            Warp& W, uint32_t fok = ~0u, const int32_t* cdep = nullptr,
+                                            Pull pull = Pull()) {
     PROF_T0(trs);
 #if SSSP_PROF
     W.prof[6]++;
@@ -517,7 +526,7 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
     for (int t = 0; t < kArcs; t++)
         old[t] = (v[t] >= 0 && (cur[t] & kVal) > c[t])
                      ? atomicCAS((unsigned long long*)(p.dist + v[t]), (unsigned long long)cur[t],
-                                 (unsigned long long)(fuses(fuse, cur[t], c[t], W) ? (c[t] | kTop) : c[t]))
+                                 (unsigned long long)(fuses(fuse && ((fok >> t) & 1), cur[t], c[t], W) ? (c[t] | kTop) : c[t]))
                      : cur[t] + 1;  // "no attempt" marker: != cur[t]
     int32_t cnt = 0, fcnt = 0;
     int out[kArcs];
@@ -527,14 +536,14 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
         if (v[t] >= 0 && (cur[t] & kVal) > c[t]) {
             if (old[t] == cur[t]) {
                 if (STATS) W.acc.succ++;
-                if (fuses(fuse, cur[t], c[t], W)) {
+                if (fuses(fuse && ((fok >> t) & 1), cur[t], c[t], W)) {
                     out[t] = kFused;
                 } else {
                     if (uses_min(POL)) W.acc.minsucc = c[t] < W.acc.minsucc ? c[t] : W.acc.minsucc;
                     out[t] = admit<STATS>(cur[t], c[t], W) ? kAppend : kNone;
                 }
             } else {
-                out[t] = write_min<POL, STATS, FUSE, BIDIR>(p.dist, v[t], c[t], old[t], fuse, W);
+                out[t] = write_min<POL, STATS, FUSE, BIDIR>(p.dist, v[t], c[t], old[t], fuse && ((fok >> t) & 1), W);
             }
         }
         cnt += out[t] == kAppend;
@@ -560,6 +569,7 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
             if (out[t] == kFused) {
                 W.fs->fid[pos] = v[t];
                 W.fs->fd[pos] = c[t];
+                W.fs->fdep[pos] = cdep[t];
                 pos++;
             }
         W.fn += tot;
@@ -583,7 +593,10 @@ __device__ __forceinline__ void relax_chunk(const RunParams& p, uint64_t d, int3
         v[t] = (int32_t)a.x;
         c[t] = d + a.y;
     }
-    relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W);
+    int32_t cd[kArcs];  // a chunk's vertex was extracted from Q: its targets lie 1 hop from it
+#pragma unroll
+    for (int t = 0; t < kArcs; t++) cd[t] = 1;
+    relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, ~0u, cd);
 }
 
 // Up to 32 vertices, one per lane (deg = 0 for none): the warp walks their
@@ -632,9 +645,11 @@ struct BidirPull {
     }
 };
 
+// FUSE kernels: `dep` = hops of this lane's vertex from its extracted seed (0 for a vertex
+// extracted from Q); a vertex it reaches may be fused only while dep + 1 <= fuse_depth.
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, int32_t beg, int32_t deg, Warp& W,
-                                               int32_t uid = -1) {
+                                               int32_t uid = -1, int32_t dep = 0) {
     const int lane = lane_id();
     if (__all_sync(kFull, deg <= kArcs)) {
         // every vertex fits one lane: lane-local arcs, no scan or owner search (fusion
@@ -651,10 +666,14 @@ __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, i
             c[t] = d + a.y;
             o[t] = lane;
         }
+        int32_t cd[kArcs];
+#pragma unroll
+        for (int t = 0; t < kArcs; t++) cd[t] = dep + 1;
+        const uint32_t fok = (FUSE && dep + 1 > p.fuse_depth) ? 0u : ~0u;
         if (BIDIR && __any_sync(kFull, uid >= 0))
-            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, BidirPull{&p, W.st->mins, o, wt, &d, uid});
+            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd, BidirPull{&p, W.st->mins, o, wt, &d, uid});
         else
-            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W);
+            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd);
         return;
     }
     int32_t total, excl;
@@ -691,10 +710,19 @@ __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, i
             wt[t] = a.y;
             c[t] = od + wt[t];
         }
+        int32_t cd[kArcs];
+        uint32_t fok = 0;
+        if (FUSE) {
+#pragma unroll
+            for (int t = 0; t < kArcs; t++) {
+                cd[t] = __shfl_sync(kFull, dep, o[t]) + 1;
+                fok |= (cd[t] <= p.fuse_depth ? 1u : 0u) << t;
+            }
+        }
         if (BIDIR && bidir)
-            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, BidirPull{&p, W.st->mins, o, wt, &d, uid_step});
+            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd, BidirPull{&p, W.st->mins, o, wt, &d, uid_step});
         else
-            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W);
+            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd);
     }
 }
 
@@ -713,11 +741,12 @@ __device__ __forceinline__ void fuse_drain(const RunParams& p, Warp& W) {
 #endif
         const int32_t cnt = W.fn < 32 ? W.fn : 32;
         __syncwarp();
-        int32_t id = -1;
+        int32_t id = -1, dep = 0;
         uint64_t d = 0;
         if (lane < cnt) {
             id = W.fs->fid[W.fn - cnt + lane];
             d = W.fs->fd[W.fn - cnt + lane];
+            dep = W.fs->fdep[W.fn - cnt + lane];
         }
         __syncwarp();
         W.fn -= cnt;
@@ -745,7 +774,7 @@ __device__ __forceinline__ void fuse_drain(const RunParams& p, Warp& W) {
                 W.acc.fused_edges += (uint64_t)deg;
             }
         }
-        relax_vertices<POL, STATS, FUSE, BIDIR>(p, d, beg, deg, W, id);
+        relax_vertices<POL, STATS, FUSE, BIDIR>(p, d, beg, deg, W, id, dep);
     }
     PROF_ADD(W, 4, tfd);
 }

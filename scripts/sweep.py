@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--no-nearfar", action="store_true", help="list all of Q every round (rho)")
     ap.add_argument("--no-fuse", action="store_true", help="no on-the-spot extraction (sparse graphs)")
     ap.add_argument("--fuse-budget", type=int, default=0)
+    ap.add_argument("--fuse-depth", type=int, default=0)
     ap.add_argument("--bidir", action="store_true", help="bidirectional relaxation (undirected graphs)")
     ap.add_argument("--trace", default=None, help="append per-round traces of the stats runs here (jsonl)")
     ap.add_argument("--tag", default=os.environ.get("SSSP_LIB", "default"))
@@ -64,7 +65,7 @@ def main():
         for pol, par in cases:
             snap = args.snapshot
             kw = dict(snapshot=snap, nearfar=not args.no_nearfar, max_rounds=200000, fuse=not args.no_fuse,
-                      fuse_budget=args.fuse_budget, bidir=args.bidir)
+                      fuse_budget=args.fuse_budget, bidir=args.bidir, fuse_depth=args.fuse_depth)
             for _ in range(2):
                 h.run(g.source, pol, par, out=d, **kw)
             ks, rs = [], []
@@ -82,7 +83,7 @@ def main():
             km = statistics.median(ks)
             bt = 8 * st["queue_scanned"] + 8 * st["dense_scanned"] + 8 * st["extracted"] + 16 * st["edges"]
             rec = {"config": name, "policy": pol, "param": par, "tag": args.tag + ("/nonf" if args.no_nearfar else "") + ("/nofuse" if args.no_fuse else "")
-                   + (f"/fb{args.fuse_budget}" if args.fuse_budget else "") + ("/bidir" if args.bidir else ""), "snapshot": snap, "kernel_ms": km, "kernel_ms_min": min(ks),
+                   + (f"/fb{args.fuse_budget}" if args.fuse_budget else "") + (f"/fd{args.fuse_depth}" if args.fuse_depth else "") + ("/bidir" if args.bidir else ""), "snapshot": snap, "kernel_ms": km, "kernel_ms_min": min(ks),
                    "gteps": g.m / km / 1e6, "rounds": statistics.median(rs), "stats_rounds": st["rounds"],
                    "bytes_touched": bt, "touched_gbs": bt / km / 1e6, "frac_6552": bt / km / 1e6 / 6552.6,
                    "edges_per_m": st["edges"] / g.m, "qscan_per_n": st["queue_scanned"] / g.n,

@@ -380,3 +380,37 @@ def test_select_exact_is_kth():
         keys = rs.integers(0, 1 << 40, size=q, dtype=np.uint64)
         rho = int(rs.integers(1, q))
         assert oracle.select_exact(keys, rho) == int(np.sort(keys)[rho - 1])
+
+
+# ----------------------------------------------------------------------------- bounded Dijkstra (bench sample)
+@pytest.mark.parametrize("name", ["rmat12", "grid64", "rgg64k"])
+def test_dijkstra_budget(name):
+    """The bounded sample bench.py times: with budget >= m it is the full Dijkstra (distances
+    equal, every reachable vertex settled once, scanned = the settled vertices' degrees); with a
+    smaller budget it stops at the first pop after the budget is reached, every settled vertex
+    is exact, and the settled ones are the closest (Dijkstra's pop order)."""
+    g = gen.make(name)
+    want = oracle.dijkstra(g)
+    deg = np.diff(g.offsets.astype(np.int64))
+    reach = want != oracle.INF
+    scanned, settled, d = oracle.dijkstra_budget(g, g.source, g.m, return_dist=True)
+    assert np.array_equal(d, want)
+    assert settled == int(reach.sum())
+    assert scanned == int(deg[reach].sum())
+    order = np.argsort(want[reach], kind="stable")
+    dr = deg[reach][order]
+    prev = 0
+    for b in (1, 7, g.m // 10, g.m // 3, g.m - 1):
+        sc, st, d = oracle.dijkstra_budget(g, g.source, b, return_dist=True)
+        assert st >= prev
+        prev = st
+        # stops at the first pop with scanned >= b: the last settled vertex pushed it over
+        assert sc >= min(b, scanned) and sc - dr[:st].max(initial=0) < b
+        # exactness of what was settled: st vertices of the true distance order carry exact values
+        exact = (d == want) & reach
+        assert exact.sum() >= st
+        # the settled set is the st closest (Dijkstra pops in distance order; ties at the
+        # st-th smallest distance kth in any order): it holds every vertex closer than kth and
+        # only vertices at most kth away, and scanned is the sum of its degrees
+        kth = np.sort(want[reach])[st - 1]
+        assert int(deg[reach][want[reach] < kth].sum()) <= sc <= int(deg[reach][want[reach] <= kth].sum())
