@@ -119,6 +119,9 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t *d_offsets, const in
                                    (DESIGN.md bidirectional)                          */
 #define SSSP_RUN_NO_NEARFAR 16u /* rho: list all of Q in the queue array every round instead of only
                                    its near part (keys <= split; DESIGN.md §5 near/far)              */
+#define SSSP_RUN_NO_SMALL 128u  /* never hand rounds to one CTA: while |Q| <= 2048 (all listed) and a
+                                   round's frontier has <= 32768 arcs, CTA 0 otherwise runs the rounds
+                                   alone with CTA barriers (DESIGN.md §5 small rounds)  */
 
 typedef struct {
     uint32_t flags;
@@ -156,6 +159,7 @@ typedef struct {
                              queue flush / fuse_drain, fuse_drain batches, relax steps,
                              SM cycles in relax steps (parts overlap: flush and relax
                              steps also count inside the relax and fuse parts)            */
+    int64_t small;        /* 1: a small-frontier round, run by CTA 0 alone                */
 } sssp_round;
 
 typedef struct {

@@ -33,7 +33,7 @@ POLICIES = {"rho": SSSP_RHO, "delta": SSSP_DELTA, "bellman_ford": SSSP_BELLMAN_F
 SSSP_VALIDATE = 1
 SSSP_NO_RELABEL = 2
 SSSP_RUN_RHO_EXACT, SSSP_RUN_NO_WARMUP, SSSP_RUN_STATS, SSSP_RUN_SNAPSHOT, SSSP_RUN_NO_NEARFAR = 1, 2, 4, 8, 16
-SSSP_RUN_NO_FUSE, SSSP_RUN_BIDIR = 32, 64
+SSSP_RUN_NO_FUSE, SSSP_RUN_BIDIR, SSSP_RUN_NO_SMALL = 32, 64, 128
 SSSP_SELECT_SAMPLED, SSSP_SELECT_EXACT = 0, 1
 
 
@@ -65,7 +65,7 @@ class sssp_run_stats(ctypes.Structure):
 ROUND_FIELDS = ["qsize", "fsize", "edges", "inserts", "succ", "theta", "nheavy", "t_theta_ns", "t_extract_ns",
                 "t_relax_ns", "qnear", "dense", "busy_a_ns", "busy_b_ns",
                 "busy_a_max_ns", "fused", "t_near_ns", "prof_scan", "prof_take", "prof_relax", "prof_flush",
-                "prof_fuse", "prof_fuse_batches", "prof_steps", "prof_step_cyc"]
+                "prof_fuse", "prof_fuse_batches", "prof_steps", "prof_step_cyc", "small"]
 ROUND_WORDS = len(ROUND_FIELDS)
 
 _vp, _i32, _i64, _u64, _u32, _sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
@@ -162,7 +162,7 @@ class SSSP:
 
     def run(self, source, policy="rho", param=0, out=None, stats=False, trace_cap=0, ext_counts=False,
             exact=False, warmup=True, seed=0, max_rounds=0, snapshot=False, nearfar=True, fuse=True,
-            fuse_budget=0, bidir=False, fuse_depth=0):
+            fuse_budget=0, bidir=False, fuse_depth=0, small=True):
         """Alg. 1 from `source`; returns a uint64-valued int64 tensor of distances (INF = -1 as int64).
 
         With stats=True returns (dist, stats_dict, trace ndarray | None, ext_count tensor | None)."""
@@ -180,7 +180,7 @@ class SSSP:
         o.flags = (SSSP_RUN_RHO_EXACT if exact else 0) | (0 if warmup else SSSP_RUN_NO_WARMUP) | \
                   (SSSP_RUN_STATS if (stats or trace_cap) else 0) | (SSSP_RUN_SNAPSHOT if snapshot else 0) | \
                   (0 if nearfar else SSSP_RUN_NO_NEARFAR) | (0 if fuse else SSSP_RUN_NO_FUSE) | \
-            (SSSP_RUN_BIDIR if bidir else 0)
+            (SSSP_RUN_BIDIR if bidir else 0) | (0 if small else SSSP_RUN_NO_SMALL)
         o.fuse_budget = fuse_budget
         o.fuse_depth = fuse_depth
         o.seed = seed

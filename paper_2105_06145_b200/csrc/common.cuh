@@ -59,6 +59,15 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned* p) {
 }
 __device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t* p) { return *(volatile const uint64_t*)p; }
 __device__ __forceinline__ int32_t ld_volatile_i32(const int32_t* p) { return *(volatile const int32_t*)p; }
+__device__ __forceinline__ int64_t ld_volatile_i64(const int64_t* p) { return *(volatile const int64_t*)p; }
+__device__ __forceinline__ int32_t ld_acquire_i32(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_i32(int32_t* p, int32_t v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ uint32_t lanemask_lt() {

@@ -143,6 +143,14 @@ struct __align__(128) Ctrl {
     int32_t pad1;
     int64_t rounds;
     int64_t tot_extracted, tot_edges, tot_succ, tot_inserts, tot_qscan, max_q, max_f, tot_dense;
+    // small-frontier rounds: the state CTA 0 hands back to the grid
+    int32_t sm_epoch;         // incremented (release) at every hand-back
+    int32_t sm_end;           // 1: the run is over (Q empty or max_rounds exceeded)
+    int64_t sm_r;             // round the grid resumes at
+    int64_t sm_qtot;          // |Q| at that round (all of it listed in the queue array)
+    uint64_t sm_theta_prev;   // Delta* / Delta-stepping: last theta
+    int32_t sm_warm;          // rho: warm-up rounds used
+    int32_t sm_rounds;        // STATS: rounds run by CTA 0
 };
 
 // A sharded append list: segment s < kShards holds [s*cap, s*cap + min(count_s, cap)),
@@ -184,6 +192,7 @@ struct RunParams {
     int32_t* counters;  // [3 slots][2 lists: queue, chunks][kSeg] * kCntStride
     uint64_t* cta_min;  // [3 slots][kMaxCtas]: per-CTA min for Delta / Dijkstra
     int64_t* cta_delta; // [3 slots][kMaxCtas]: per-CTA change of |Q| (inserts - extractions)
+    int32_t* cta_ext;   // [3 slots][kMaxCtas]: per-CTA extractions (fusion included)
     Desc* light;
     uint64_t* samples;
     Ctrl* ctrl;
@@ -301,7 +310,16 @@ __device__ __forceinline__ int seg_of(const int64_t* pref, int64_t i) {
 
 // --------------------------------------------------------------------- per-warp staging
 constexpr int kPend = 64;  // deferred WriteMins: pending WriteMins per warp (drained at 32)
+// (a kernel unit is compiled for one fusion flag, INST_FUSE; run.cu sees neither)
+#if defined(INST_FUSE) && INST_FUSE
+#define SSSP_FUSE_UNIT 1
+#else
+#define SSSP_FUSE_UNIT 0
+#endif
 struct WarpStage {
+#if !SSSP_FUSE_UNIT
+    int32_t ext;          // vertices this warp extracted this round (lane 0 counts; small-round entry test)
+#endif
     int32_t take[kTBuf];  // ids that pass the theta test, extracted 32 at a time
     int32_t q[kQBuf];     // ids appended to the next queue
     uint64_t mins[32];    // bidirectional relaxation: per-vertex pulled minimum
@@ -315,9 +333,51 @@ struct FuseStage {        // FUSE kernels only (kept out of the others' shared m
     int32_t fdep[kFBuf];  // ... and hops from the extracted seed
 };
 
+// --------------------------------------------------------------------- small-frontier rounds
+// While |Q| <= kSmallQ (all of it listed) and a round's frontier has at most kSmallArcs arcs,
+// CTA 0 runs the rounds alone with CTA barriers and the queue in shared memory; the other
+// CTAs wait on a flag (DESIGN.md §5 "small-frontier rounds"; the paper's "insufficient
+// workload and thus overhead in the synchronization cost").
+#ifndef SSSP_SMALL
+#define SSSP_SMALL 1  // 0: compile the small-frontier path out (A/B builds)
+#endif
+// Kernels with fusion do not run small rounds: there a small |Q| hides the fused work, and the
+// path cost them 3-6 % (A/B on grid256 / grid4096 / rgg4m); the others gain from it.
+__host__ __device__ constexpr bool small_on(bool fuse) { return SSSP_SMALL && !fuse; }
+constexpr int kSmallQ = 2048;
+constexpr int kSmallArcs = 32768;
+#ifndef SSSP_SMALL_F
+#define SSSP_SMALL_F 256
+#endif
+constexpr int kSmallF = SSSP_SMALL_F;  // ... entered only after a round that extracted at most this many
+                               // vertices (fusion included), left after one that extracted more
+                               // than 2 kSmallF: on road graphs a small |Q| can still fuse tens of
+                               // thousands of vertices per round, more than one SM should take
+static_assert(kSmallQ % kBlock == 0, "small-round queue: whole entries per thread");
+struct SmallSmem {
+    int32_t q[2][kSmallQ];     // Q_r / Q_{r+1} ids (entries >= kSmallQ of Q_{r+1} go to gq)
+    int32_t qcnt[2];
+    int32_t on;                // 1 while CTA 0 runs small rounds: wq_flush appends here
+    int32_t nxt;               // which q[] receives Q_{r+1}
+    int32_t* gq;               // Q_{r+1} in the grid's flat layout (overflow, and the hand-back)
+    int64_t qcap;
+    unsigned long long arcs;   // arcs of the round's frontier
+    int32_t heavy;             // a vertex of degree > kLight was extracted (chunk list in use)
+    int32_t ext;               // vertices extracted this round (fusion included)
+};
+#if !SSSP_FUSE_UNIT
+__shared__ SmallSmem s_small;
+#endif
+
+// i-th entry of a queue buffer seen as one flat list: shard-0 segment, then the spill segment
+__device__ __forceinline__ int32_t* flat_slot(int32_t* base, int64_t qcap, int64_t i) {
+    return i < qcap ? base + i : base + (int64_t)kShards * qcap + (i - qcap);
+}
+
 // dynamic shared memory: per-warp stages, theta samples, select scratch [, fuse stages]
 constexpr size_t kSmemBase = (kWarps * sizeof(WarpStage) + kSmemSamples * sizeof(uint64_t) + sizeof(SelectSmem) + 15) /
                              16 * 16;
+extern __shared__ __align__(16) unsigned char sssp_dyn_smem[];
 
 struct Acc {
     uint64_t minsucc = kInf;
@@ -327,20 +387,76 @@ struct Acc {
     uint64_t fused_edges = 0;  // STATS: their arcs
 };
 
-struct Warp {  // per-warp working state (qn is warp-uniform)
-    WarpStage* st;
-    FuseStage* fs;
-    Sharded<int32_t> qnext;
-    RoundCnt* C;
+// Per-round values every warp of a CTA reads.  Kernels without fusion keep them in shared
+// memory (written by thread 0 before a CTA barrier), not in each thread's registers: they run
+// at 64 registers, and this cold state cost them spills in their hot loops (Bellman-Ford on
+// rmat24 +16 % with the small-round path).  The fusion kernels, whose hops are latency chains,
+// keep the round-1 layout: per-thread registers (A/B: 3-12 % slower from shared memory).
+struct RoundSmem {
+    Sharded<int32_t> qnext;  // the list WriteMins append Q_{r+1}'s near part to
+    RoundCnt* C;             // this round's counters (STATS, snapshot light list)
+};
+__shared__ RoundSmem s_rnd;
+
+struct Warp {  // per-warp working state in registers (qn, fn, pn are warp-uniform)
+#if SSSP_FUSE_UNIT
+    WarpStage* st_;
+    FuseStage* fs_;
+    Sharded<int32_t> qnext_;
+    RoundCnt* C_;
+    int shard_;
+    __device__ __forceinline__ WarpStage* st() const { return st_; }
+    __device__ __forceinline__ FuseStage* fs() const { return fs_; }
+    __device__ __forceinline__ const Sharded<int32_t>& qnext() const { return qnext_; }
+    __device__ __forceinline__ RoundCnt* C() const { return C_; }
+    __device__ __forceinline__ int shard() const { return shard_; }
+    __device__ __forceinline__ void init() {
+        st_ = (WarpStage*)sssp_dyn_smem + (threadIdx.x >> 5);
+        fs_ = (FuseStage*)(sssp_dyn_smem + kSmemBase) + (threadIdx.x >> 5);
+        shard_ = (int)(warp_rank() % kShards);
+    }
+    // every thread, at the round top
+    __device__ __forceinline__ void set_round(const Sharded<int32_t>& q, RoundCnt* c) {
+        qnext_ = q;
+        C_ = c;
+    }
+    __device__ __forceinline__ Sharded<int32_t> swap_qnext(const Sharded<int32_t>& q) {  // all threads
+        const Sharded<int32_t> o = qnext_;
+        qnext_ = q;
+        return o;
+    }
+#else
+    __device__ __forceinline__ WarpStage* st() const { return (WarpStage*)sssp_dyn_smem + (threadIdx.x >> 5); }
+    __device__ __forceinline__ FuseStage* fs() const {
+        return (FuseStage*)(sssp_dyn_smem + kSmemBase) + (threadIdx.x >> 5);
+    }
+    __device__ __forceinline__ const Sharded<int32_t>& qnext() const { return s_rnd.qnext; }
+    __device__ __forceinline__ RoundCnt* C() const { return s_rnd.C; }
+    __device__ __forceinline__ int shard() const { return (int)(warp_rank() % kShards); }
+    __device__ __forceinline__ void init() {}
+    // every thread, at the round top, before a CTA barrier
+    __device__ __forceinline__ void set_round(const Sharded<int32_t>& q, RoundCnt* c) {
+        if (threadIdx.x == 0) {
+            s_rnd.qnext = q;
+            s_rnd.C = c;
+        }
+    }
+    __device__ __forceinline__ Sharded<int32_t> swap_qnext(const Sharded<int32_t>& q) {  // all threads
+        Sharded<int32_t> o = s_rnd.qnext;
+        __syncthreads();
+        if (threadIdx.x == 0) s_rnd.qnext = q;
+        __syncthreads();
+        return o;
+    }
+#endif
     uint64_t split;       // near/far split: keys <= split are held in the queue array
     uint64_t fuse_theta;  // live rounds: theta (a vertex outside Q improved to <= theta is
                           // extracted on the spot, DESIGN.md §5 "fusion"); 0 = no fusion
     int64_t qdelta;       // this lane's inserts - extractions (|Q| bookkeeping)
-    int shard;
     int32_t qn;
     int32_t fn;       // staged fused vertices (warp-uniform)
     int32_t fbudget;  // fusions left this round (warp-uniform)
-    int32_t pn;       // deferred WriteMins: pending WriteMins (warp-uniform)
+    int32_t pn;       // deferred WriteMins: pending (warp-uniform)
     Acc acc;
 #if SSSP_PROF
     // cycles in scan, take, light relax, queue flush, fuse_drain; fuse_drain batches;
@@ -399,11 +515,29 @@ __device__ __forceinline__ void wq_flush(Warp& W) {
     if (W.qn == 0) return;
     PROF_T0(tf);
     __syncwarp();
+#if !SSSP_FUSE_UNIT
+    if (s_small.on) {  // small-frontier rounds (CTA 0 alone): Q_{r+1} in shared memory
+        int32_t pos = 0;
+        if (lane_id() == 0) pos = atomicAdd(&s_small.qcnt[s_small.nxt], W.qn);
+        pos = __shfl_sync(kFull, pos, 0);
+        int32_t* sq = s_small.q[s_small.nxt];
+        for (int32_t i = lane_id(); i < W.qn; i += 32) {
+            const int32_t v = W.st()->q[i], j = pos + i;
+            if (j < kSmallQ)
+                sq[j] = v;
+            else
+                *flat_slot(s_small.gq, s_small.qcap, j) = v;
+        }
+        __syncwarp();
+        W.qn = 0;
+        return;
+    }
+#endif
     int32_t *p0, *p1;
     int32_t fit, lim;
-    reserve(W.qnext, W.shard, W.qn, p0, fit, p1, lim);
+    reserve(W.qnext(), W.shard(), W.qn, p0, fit, p1, lim);
     for (int32_t i = lane_id(); i < lim; i += 32) {
-        const int32_t v = W.st->q[i];
+        const int32_t v = W.st()->q[i];
         if (i < fit)
             p0[i] = v;
         else
@@ -420,7 +554,7 @@ __device__ __forceinline__ void wq_push1(Warp& W, bool pred, int32_t id) {
     if (!mask) return;
     const int32_t cnt = __popc(mask);
     if (W.qn + cnt > kQBuf) wq_flush(W);
-    if (pred) W.st->q[W.qn + __popc(mask & lanemask_lt())] = id;
+    if (pred) W.st()->q[W.qn + __popc(mask & lanemask_lt())] = id;
     W.qn += cnt;
 }
 
@@ -465,8 +599,8 @@ __device__ __forceinline__ void run_pending(const RunParams& p, Warp& W, int32_t
     int32_t v = -1;
     if (lane < cnt) {
         const int32_t j = W.pn - cnt + lane;
-        v = W.st->pv[j];
-        out = write_min<POL, STATS, FUSE, BIDIR>(p.dist, v, W.st->pc[j], W.st->pw[j], false, W);
+        v = W.st()->pv[j];
+        out = write_min<POL, STATS, FUSE, BIDIR>(p.dist, v, W.st()->pc[j], W.st()->pw[j], false, W);
     }
     __syncwarp();
     W.pn -= cnt;
@@ -509,9 +643,9 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
             if (!m) continue;
             if (imp) {
                 const int32_t j = W.pn + __popc(m & lanemask_lt());
-                W.st->pv[j] = v[t];
-                W.st->pc[j] = c[t];
-                W.st->pw[j] = cur[t];
+                W.st()->pv[j] = v[t];
+                W.st()->pc[j] = c[t];
+                W.st()->pw[j] = cur[t];
             }
             W.pn += __popc(m);
             if (W.pn >= 32) run_pending<POL, STATS, FUSE, BIDIR>(p, W, 32);
@@ -557,7 +691,7 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
         int32_t pos = W.qn + excl;
 #pragma unroll
         for (int t = 0; t < kArcs; t++)
-            if (out[t] == kAppend) W.st->q[pos++] = v[t];
+            if (out[t] == kAppend) W.st()->q[pos++] = v[t];
         W.qn += tot;
     }
     if (FUSE && fuse && __any_sync(kFull, fcnt != 0)) {
@@ -567,9 +701,9 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
 #pragma unroll
         for (int t = 0; t < kArcs; t++)
             if (out[t] == kFused) {
-                W.fs->fid[pos] = v[t];
-                W.fs->fd[pos] = c[t];
-                W.fs->fdep[pos] = cdep[t];
+                W.fs()->fid[pos] = v[t];
+                W.fs()->fd[pos] = c[t];
+                W.fs()->fdep[pos] = cdep[t];
                 pos++;
             }
         W.fn += tot;
@@ -671,7 +805,7 @@ __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, i
         for (int t = 0; t < kArcs; t++) cd[t] = dep + 1;
         const uint32_t fok = (FUSE && dep + 1 > p.fuse_depth) ? 0u : ~0u;
         if (BIDIR && __any_sync(kFull, uid >= 0))
-            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd, BidirPull{&p, W.st->mins, o, wt, &d, uid});
+            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd, BidirPull{&p, W.st()->mins, o, wt, &d, uid});
         else
             relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd);
         return;
@@ -720,7 +854,7 @@ __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, i
             }
         }
         if (BIDIR && bidir)
-            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd, BidirPull{&p, W.st->mins, o, wt, &d, uid_step});
+            relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd, BidirPull{&p, W.st()->mins, o, wt, &d, uid_step});
         else
             relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd);
     }
@@ -744,9 +878,9 @@ __device__ __forceinline__ void fuse_drain(const RunParams& p, Warp& W) {
         int32_t id = -1, dep = 0;
         uint64_t d = 0;
         if (lane < cnt) {
-            id = W.fs->fid[W.fn - cnt + lane];
-            d = W.fs->fd[W.fn - cnt + lane];
-            dep = W.fs->fdep[W.fn - cnt + lane];
+            id = W.fs()->fid[W.fn - cnt + lane];
+            d = W.fs()->fd[W.fn - cnt + lane];
+            dep = W.fs()->fdep[W.fn - cnt + lane];
         }
         __syncwarp();
         W.fn -= cnt;
@@ -826,7 +960,7 @@ __device__ __forceinline__ void take_batch(const RunParams& p, int32_t cnt, cons
     const int lane = lane_id();
     PROF_T0(tt);
     __syncwarp();
-    int32_t id = lane < cnt ? W.st->take[lane] : -1;
+    int32_t id = lane < cnt ? W.st()->take[lane] : -1;
     // the CSR row is read alongside the delete (independent loads: one latency, not two);
     // the results are consumed by selects, not inside the branch, so they stay ahead of it
     int32_t beg = 0, end = 0;
@@ -840,6 +974,12 @@ __device__ __forceinline__ void take_batch(const RunParams& p, int32_t cnt, cons
     const int32_t deg = ok ? end - beg : 0;
     beg = ok ? beg : 0;
     id = ok ? id : -1;
+    {
+        const uint32_t em = __ballot_sync(kFull, id >= 0);
+#if !SSSP_FUSE_UNIT
+        if (small_on(FUSE) && lane == 0) W.st()->ext += __popc(em);
+#endif
+    }
     if (id >= 0) {
         W.qdelta--;
         if (p.ext_count) atomicAdd(p.ext_count + (p.ofno ? p.ofno[id] : id), 1);
@@ -850,9 +990,9 @@ __device__ __forceinline__ void take_batch(const RunParams& p, int32_t cnt, cons
     }
     const bool heavy = deg > kLight;
     const bool light = id >= 0 && deg > 0 && !heavy;
-    emit_chunks(CL, W.shard, heavy, d, beg, deg, W.C, STATS);
+    emit_chunks(CL, W.shard(), heavy, d, beg, deg, W.C(), STATS);
     if (snap) {
-        const int32_t ls = warp_append_slot(light, &W.C->nlight);
+        const int32_t ls = warp_append_slot(light, &W.C()->nlight);
         if (light) st_desc(p.light + ls, d, beg, deg);
     } else if (__any_sync(kFull, light)) {
         PROF_ADD(W, 1, tt);
@@ -930,7 +1070,7 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
             wq_push1(W, rem && val[e] <= W.split, id[e]);  // above the split: stays in Q as a far member
             if (uses_min(POL) && rem) minrem = val[e] < minrem ? val[e] : minrem;
             const uint32_t tm = __ballot_sync(kFull, take);
-            if (take) W.st->take[tn + __popc(tm & lanemask_lt())] = id[e];
+            if (take) W.st()->take[tn + __popc(tm & lanemask_lt())] = id[e];
             tn += __popc(tm);
         }
         PROF_ADD(W, 0, ts);
@@ -938,9 +1078,9 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
         while (tn - done >= 32) {
             if (done) {  // move the next 32 to the front (take_batch reads take[0..32))
                 __syncwarp();
-                const int32_t x = W.st->take[done + lane];
+                const int32_t x = W.st()->take[done + lane];
                 __syncwarp();
-                W.st->take[lane] = x;
+                W.st()->take[lane] = x;
             }
             take_batch<POL, STATS, FUSE, BIDIR>(p, 32, CL, snap, W, fs, edges);
             done += 32;
@@ -949,9 +1089,9 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
             __syncwarp();
             const bool mv = lane < tn - done;
             int32_t x = 0;
-            if (mv) x = W.st->take[done + lane];
+            if (mv) x = W.st()->take[done + lane];
             __syncwarp();
-            if (mv) W.st->take[lane] = x;
+            if (mv) W.st()->take[lane] = x;
             tn -= done;
         }
     }
@@ -960,18 +1100,16 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
     if (STATS) {
         fs = warp_sum(fs);
         edges = warp_sum(edges);
-        if (lane == 0 && fs) atomicAdd(&W.C->fsize, (unsigned long long)fs);
-        if (lane == 0 && edges) atomicAdd(&W.C->edges, (unsigned long long)edges);
+        if (lane == 0 && fs) atomicAdd(&W.C()->fsize, (unsigned long long)fs);
+        if (lane == 0 && edges) atomicAdd(&W.C()->edges, (unsigned long long)edges);
     }
 }
 
 // --------------------------------------------------------------------- phase B
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __device__ __forceinline__ void phase_b(const RunParams& p, const Sharded<Desc>& CL, const int64_t* cpref, int32_t nl,
-                                        Warp& W) {
+                                        Warp& W, int64_t gw, int64_t nwarps) {
     const int lane = lane_id();
-    const int64_t gw = warp_rank();
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nb = ((int64_t)nl + 31) / 32;
     const int64_t nc = cpref[kSeg];
     const int64_t total = nb + nc;
@@ -1018,14 +1156,20 @@ __device__ __forceinline__ void flush_acc(const RunParams& p, int64_t r, Warp& W
     if (lane_id() == 0 && dq) atomicAdd((unsigned long long*)(p.cta_delta + (r % 3) * kMaxCtas + blockIdx.x),
                                         (unsigned long long)dq);
     W.qdelta = 0;
+#if !SSSP_FUSE_UNIT
+    if (small_on(FUSE) && lane_id() == 0 && W.st()->ext) {
+        atomicAdd(p.cta_ext + (r % 3) * kMaxCtas + blockIdx.x, W.st()->ext);
+        W.st()->ext = 0;
+    }
+#endif
     if (STATS) {
         const uint32_t s = warp_sum(W.acc.succ), ins = warp_sum(W.acc.inserts), fu = warp_sum(W.acc.fused);
         const uint64_t fe = warp_sum(W.acc.fused_edges);
-        if (lane_id() == 0 && s) atomicAdd(&W.C->succ, (unsigned long long)s);
-        if (lane_id() == 0 && ins) atomicAdd(&W.C->inserts, (unsigned long long)ins);
-        if (lane_id() == 0 && fu) atomicAdd(&W.C->fsize, (unsigned long long)fu);
-        if (lane_id() == 0 && fu) atomicAdd(&W.C->fused, (unsigned long long)fu);
-        if (lane_id() == 0 && fe) atomicAdd(&W.C->edges, (unsigned long long)fe);
+        if (lane_id() == 0 && s) atomicAdd(&W.C()->succ, (unsigned long long)s);
+        if (lane_id() == 0 && ins) atomicAdd(&W.C()->inserts, (unsigned long long)ins);
+        if (lane_id() == 0 && fu) atomicAdd(&W.C()->fsize, (unsigned long long)fu);
+        if (lane_id() == 0 && fu) atomicAdd(&W.C()->fused, (unsigned long long)fu);
+        if (lane_id() == 0 && fe) atomicAdd(&W.C()->edges, (unsigned long long)fe);
     }
     W.acc.succ = 0;
     W.acc.inserts = 0;
@@ -1094,8 +1238,7 @@ __device__ __forceinline__ uint64_t cta_kth_by_rank(const uint64_t* keys, int s,
 __device__ __forceinline__ void far_to_near(const RunParams& p, const Sharded<int32_t>& L, uint64_t lo, uint64_t hi,
                                             Warp& W) {
     const int lane = lane_id();
-    const Sharded<int32_t> saved = W.qnext;
-    W.qnext = L;
+    const Sharded<int32_t> saved = W.swap_qnext(L);
     const int64_t gw = warp_rank();
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     constexpr int kV = 8;
@@ -1113,7 +1256,7 @@ __device__ __forceinline__ void far_to_near(const RunParams& p, const Sharded<in
         }
     }
     wq_flush(W);
-    W.qnext = saved;
+    W.swap_qnext(saved);
 }
 
 // CTA-0 estimate of the value below which about `want` far members lie: rejection-sample
@@ -1136,10 +1279,329 @@ static __device__ __forceinline__ uint64_t far_quantile(const RunParams& p, uint
     return h <= kRankSelect ? cta_kth_by_rank(keys, h, k, sm) : cta_kth_smallest(SmemKey{keys}, h, k, sm);
 }
 
+// --------------------------------------------------------------------- small-frontier rounds
+struct SmallKey {  // key of the i-th id of a shared-memory queue
+    const int32_t* q;
+    const uint64_t* dist;
+    __device__ uint64_t operator()(int64_t i) const { return ld_cg_u64(dist + q[i]) & kVal; }
+};
+__device__ __forceinline__ uint64_t atom_and_u64(uint64_t* p, uint64_t x) {
+    uint64_t old;
+    asm volatile("atom.global.and.b64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(x) : "memory");
+    return old;
+}
+// theta_i = i * Delta, skipping empty steps (reading R2), saturating
+__device__ __forceinline__ uint64_t delta_next(uint64_t theta_prev, uint64_t minq, uint64_t D) {
+    const uint64_t x = theta_prev > kInf - D ? kInf : theta_prev + D;
+    const uint64_t y = (minq / D + (minq % D != 0)) * D;
+    return x > y ? x : y;
+}
+
+#if !SSSP_FUSE_UNIT
+// Rounds r, r+1, ... of Alg. 1 run by CTA 0 alone (all 1024 threads call it), starting from
+// Q_r (|Q_r| = qtot <= kSmallQ ids, all listed in the grid's queue QC0 / qpref0).  Each round:
+//   ExtDist per policy (as the grid computes it, over all of Q);
+//   Extract: every queued id is deleted by atomicOr (which returns its key) and its CSR row
+//            read alongside; ids above theta are put back (atomicAnd) and kept;   CTA barrier
+//   if the frontier has more than kSmallArcs arcs: undo the round and hand it to the grid;
+//   Relax: light vertices by the warp that holds them, heavy ones as chunk descriptors that
+//          all 32 warps stride over (phase_b); WriteMins append to Q_{r+1} in shared memory;
+//          fusion as in the grid's live rounds.                               CTA barrier
+// Every round extracts before it relaxes, with the keys Extract returned: the LaB-PQ's
+// exclusive Extract, i.e. the grid's snapshot rounds.  Returns when Q is empty,
+// |Q| > kSmallQ, or a frontier is too large; Q is then written back in the grid's layout and
+// the resume state to ctrl (sm_*); the caller releases the other CTAs.
+template <int POL, bool STATS, bool FUSE, bool BIDIR>
+__device__ __forceinline__ void small_rounds(const RunParams& p, int64_t r, int64_t qtot, uint64_t theta_prev, int warm, uint64_t minq,
+                  const Sharded<int32_t> QC0, const int64_t* qpref0, int64_t* cpref, uint64_t* red) {
+    // (inlined outside the grid's round loop; a __noinline__ version, which must read the
+    // parameters through a global copy, was 4-20 % slower per small round)
+    constexpr int kE = kSmallQ / kBlock;  // queue entries per thread
+    const int tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
+    uint64_t* s_keys = (uint64_t*)(sssp_dyn_smem + kWarps * sizeof(WarpStage));
+    SelectSmem& sm = *(SelectSmem*)(s_keys + kSmemSamples);
+    Warp W;  // this warp's state for the small rounds (the grid's is empty between rounds)
+    W.init();
+    W.qn = W.fn = W.pn = 0;
+    W.qdelta = 0;
+#if SSSP_PROF
+    for (int i = 0; i < kProf; i++) W.prof[i] = 0;
+#endif
+    Ctrl* ctrl = p.ctrl;
+    const bool snap = (p.flags & SSSP_RUN_SNAPSHOT) != 0;
+    const int64_t qcap = p.qcap;
+    for (int64_t i = tid; i < qtot; i += blockDim.x) {
+        const int sg = seg_of(qpref0, i);
+        s_small.q[0][i] = ld_cg_i32(QC0.seg(sg) + (i - qpref0[sg]));
+    }
+    if (tid == 0) {
+        s_small.on = 1;
+        s_small.qcnt[0] = (int32_t)qtot;
+        s_small.qcap = qcap;
+    }
+    W.split = kInf;
+    W.fuse_theta = 0;
+    int cur = 0;
+    int end = 0;  // 1: Q empty / rounds exceeded; 2: Q_r handed to the grid
+    int32_t last_ext = 0;  // extractions of the last round run here (the grid's entry test)
+    __syncthreads();
+    for (;;) {
+        if (r > p.max_rounds) {
+            if (tid == 0) ctrl->status = SSSP_ERR_ROUNDS;
+            end = 1;
+            break;
+        }
+        RoundCnt* C = &ctrl->cnt[r % 3];
+        uint64_t t0 = 0, t1 = 0, t2 = 0;
+        if (STATS && tid == 0) t0 = globaltimer();
+        const int32_t* q = s_small.q[cur];
+        const int32_t qn = (int32_t)qtot;
+        const uint64_t theta_prev0 = theta_prev;  // (restored if the round is handed to the grid)
+        const int warm0 = warm;
+        // ---- ExtDist (Table tab:framework), over all of Q
+        uint64_t theta;
+        if (POL == SSSP_BELLMAN_FORD) {
+            theta = kInf;
+        } else if (POL == SSSP_DIJKSTRA) {
+            theta = minq;
+        } else if (POL == SSSP_DELTA_STEPPING && r > 1 && minq <= theta_prev) {
+            theta = theta_prev;  // FinishCheck failed (R19)
+        } else if (POL == SSSP_DELTA || POL == SSSP_DELTA_STEPPING) {
+            theta = delta_next(theta_prev, minq, p.param);
+            theta_prev = theta;
+        } else {  // rho
+            uint64_t rho = p.param;
+            if (!(p.flags & SSSP_RUN_NO_WARMUP) && (uint64_t)qtot > rho && warm < 2) {
+                warm++;
+                rho = rho / 10 ? rho / 10 : 1;  // reading R7
+            }
+            if ((uint64_t)qtot <= rho) {
+                theta = kInf;
+            } else if (p.flags & SSSP_RUN_RHO_EXACT) {
+                theta = cta_kth_smallest(SmallKey{q, p.dist}, qtot, rho, sm);
+            } else {
+                const uint64_t sc = sample_count((uint64_t)qtot, rho);
+                uint64_t* keys = sc <= (uint64_t)kSmemSamples ? s_keys : p.samples;
+                for (uint64_t j = tid; j < sc; j += blockDim.x)
+                    keys[j] = ld_cg_u64(p.dist + q[sample_index(p.seed, r, j, (uint64_t)qtot)]) & kVal;
+                __syncthreads();
+                uint64_t k = (rho * sc + (uint64_t)qtot - 1) / (uint64_t)qtot;
+                k = k < 1 ? 1 : (k > sc ? sc : k);
+                theta = sc <= (uint64_t)kRankSelect ? cta_kth_by_rank(keys, (int)sc, k, sm)
+                                                    : cta_kth_smallest(ArrayKey{keys}, (int64_t)sc, k, sm);
+            }
+        }
+        if (STATS && tid == 0) t1 = globaltimer();
+        const int nxt = cur ^ 1;
+        if (tid < 2 * kSeg)  // counters of slot (r+1)%3 (the chunk list of round r+1)
+            p.counters[((int64_t)(((r + 1) % 3) * 2) * kSeg + tid) * kCntStride] = 0;
+        if (tid == 0) {
+            reset_cnt(&ctrl->cnt[(r + 1) % 3]);
+            s_small.qcnt[nxt] = 0;
+            s_small.nxt = nxt;
+            s_small.gq = p.qbuf[(r + 1) & 1];
+            s_small.arcs = 0;
+            s_small.heavy = 0;
+            s_small.ext = 0;
+        }
+        W.set_round(s_rnd.qnext, C);  // (C: thread 0, before the barrier below)
+        W.fuse_theta = (FUSE && !snap) ? theta : 0;
+        __syncthreads();
+        // ---- Extract(theta): delete every queued id, keep those above theta
+        int32_t id[kE], beg[kE], deg[kE];
+        uint64_t d[kE];
+        bool keep[kE];
+        uint64_t minrem = kInf;
+        unsigned long long arcs = 0;
+#pragma unroll
+        for (int e = 0; e < kE; e++) {
+            const int i = e * kBlock + tid;
+            id[e] = -1;
+            deg[e] = 0;
+            beg[e] = 0;
+            d[e] = 0;
+            keep[e] = false;
+            if (i < qn) {
+                const int32_t v = q[i];
+                int32_t b, en;
+                ld_row(p.off, v, b, en);
+                const uint64_t old = atom_or_u64(p.dist + v, kTop);
+                const uint64_t key = old & kVal;
+                if (!(old & kTop)) {  // (every listed id is in Q; a deleted one is skipped)
+                    if (key <= theta) {
+                        id[e] = v;
+                        d[e] = key;
+                        beg[e] = b;
+                        deg[e] = en - b;
+                        arcs += (unsigned long long)(en - b);
+                    } else {
+                        atom_and_u64(p.dist + v, ~kTop);  // back into Q (no WriteMin runs yet)
+                        minrem = key < minrem ? key : minrem;
+                        keep[e] = true;
+                    }
+                }
+            }
+        }
+        arcs = warp_sum(arcs);
+        if (lane == 0 && arcs) atomicAdd(&s_small.arcs, arcs);
+        __syncthreads();
+        if (s_small.arcs > (unsigned long long)kSmallArcs) {
+            // too much work for one SM: undo the deletions and hand round r to the grid
+#pragma unroll
+            for (int e = 0; e < kE; e++)
+                if (id[e] >= 0) atom_and_u64(p.dist + id[e], ~kTop);
+            theta_prev = theta_prev0;
+            warm = warm0;
+            end = 2;
+            break;
+        }
+        // kept ids go to Q_{r+1} first (in queue order)
+#pragma unroll
+        for (int e = 0; e < kE; e++) wq_push1(W, keep[e], keep[e] ? q[e * kBlock + tid] : -1);
+        int64_t fs = 0;
+#pragma unroll
+        for (int e = 0; e < kE; e++) {
+            const uint32_t em = __ballot_sync(kFull, id[e] >= 0);
+            if (lane == 0) W.st()->ext += __popc(em);
+        }
+#pragma unroll
+        for (int e = 0; e < kE; e++)
+            if (id[e] >= 0) {
+                fs++;
+                if (p.ext_count) atomicAdd(p.ext_count + (p.ofno ? p.ofno[id[e]] : id[e]), 1);
+            }
+        if (STATS) {
+            fs = warp_sum(fs);
+            const unsigned long long a = arcs;
+            if (lane == 0 && fs) atomicAdd(&C->fsize, (unsigned long long)fs);
+            if (lane == 0 && a) atomicAdd(&C->edges, a);
+        }
+        // ---- Relax (with the keys Extract returned)
+        W.fbudget = p.fuse_budget;
+        const Sharded<Desc> CL = chunks_of(p, r);
+#pragma unroll
+        for (int e = 0; e < kE; e++) {
+            const bool heavy = deg[e] > kLight;
+            const bool light = id[e] >= 0 && deg[e] > 0 && !heavy;
+            if (__any_sync(kFull, heavy)) {
+                if (lane == 0) s_small.heavy = 1;
+                emit_chunks(CL, W.shard(), heavy, d[e], beg[e], deg[e], C, STATS);
+            }
+            if (__any_sync(kFull, light))
+                relax_vertices<POL, STATS, FUSE, BIDIR>(p, d[e], beg[e], light ? deg[e] : 0, W, light ? id[e] : -1);
+        }
+        fuse_drain<POL, STATS, FUSE, BIDIR>(p, W);
+        __syncthreads();
+        if (s_small.heavy) {  // heavy vertices: all warps of the CTA stride over their chunks
+            load_prefix(CL, cpref);
+            phase_b<POL, STATS, FUSE, BIDIR>(p, CL, cpref, 0, W, wid, kWarps);
+        }
+        drain_pending<POL, STATS, FUSE, BIDIR>(p, W);
+        wq_flush(W);
+        if (STATS) {
+            const uint32_t sc = warp_sum(W.acc.succ), ins = warp_sum(W.acc.inserts), fu = warp_sum(W.acc.fused);
+            const uint64_t fe = warp_sum(W.acc.fused_edges);
+            if (lane == 0 && sc) atomicAdd(&C->succ, (unsigned long long)sc);
+            if (lane == 0 && ins) atomicAdd(&C->inserts, (unsigned long long)ins);
+            if (lane == 0 && fu) atomicAdd(&C->fsize, (unsigned long long)fu);
+            if (lane == 0 && fu) atomicAdd(&C->fused, (unsigned long long)fu);
+            if (lane == 0 && fe) atomicAdd(&C->edges, (unsigned long long)fe);
+            W.acc.succ = W.acc.inserts = W.acc.fused = 0;
+            W.acc.fused_edges = 0;
+        }
+        // min_Q delta of Q_{r+1}: kept keys and successful WriteMins (Delta* / Dijkstra)
+        if (uses_min(POL)) {
+            const uint64_t mn = warp_min_u64(minrem < W.acc.minsucc ? minrem : W.acc.minsucc);
+            if (lane == 0) red[wid] = mn;
+            W.acc.minsucc = kInf;
+        }
+        W.qdelta = 0;
+        if (lane == 0 && W.st()->ext) {
+            atomicAdd(&s_small.ext, W.st()->ext);
+            W.st()->ext = 0;
+        }
+        __syncthreads();
+        const int32_t ext = s_small.ext;
+        if (uses_min(POL)) {
+            uint64_t mn = kInf;
+            for (int i = 0; i < kWarps; i++) mn = red[i] < mn ? red[i] : mn;
+            minq = mn;
+        }
+        const int64_t qnext = s_small.qcnt[nxt];
+        if (STATS && tid == 0) {
+            t2 = globaltimer();
+            const int64_t f = (int64_t)C->fsize;
+            if (p.trace && r - 1 < p.trace_cap) {
+                sssp_round* t = p.trace + (r - 1);
+                memset(t, 0, sizeof(*t));
+                t->qsize = qtot;
+                t->fsize = f;
+                t->edges = (int64_t)C->edges;
+                t->inserts = (int64_t)C->inserts;
+                t->succ = (int64_t)C->succ;
+                t->theta = theta;
+                t->nheavy = (int64_t)C->nheavy;
+                t->t_theta_ns = (int64_t)(t1 - t0);
+                t->t_extract_ns = (int64_t)(t2 - t1);
+                t->qnear = qtot;
+                t->fused = (int64_t)C->fused;
+                t->small = 1;
+            }
+            ctrl->tot_extracted += f;
+            ctrl->tot_edges += (int64_t)C->edges;
+            ctrl->tot_succ += (int64_t)C->succ;
+            ctrl->tot_inserts += (int64_t)C->inserts;
+            ctrl->tot_qscan += qtot;
+            ctrl->max_q = qtot > ctrl->max_q ? qtot : ctrl->max_q;
+            ctrl->max_f = f > ctrl->max_f ? f : ctrl->max_f;
+            ctrl->sm_rounds++;
+        }
+        r++;
+        qtot = qnext;
+        cur = nxt;
+        if (qtot == 0) {
+            end = 1;
+            break;
+        }
+        if (qtot > kSmallQ || ext > 2 * kSmallF) {
+            last_ext = ext;
+            end = 2;
+            break;
+        }
+        __syncthreads();  // (the next round reuses the other queue buffer and s_small fields)
+    }
+    // ---- hand back: Q_r in the grid's layout (flat: shard-0 segment, then the spill segment)
+    if (end == 2) {
+        int32_t* gq = p.qbuf[r & 1];
+        const int64_t ns = qtot < kSmallQ ? qtot : kSmallQ;  // the rest is in gq already
+        for (int64_t i = tid; i < ns; i += blockDim.x) *flat_slot(gq, qcap, i) = s_small.q[cur][i];
+        // queue counts of Q_r: slot (r+2)%3, list 0
+        int32_t* qc = p.counters + (int64_t)((((r + 2) % 3) * 2) * kSeg) * kCntStride;
+        if (tid < kSeg)
+            qc[tid * kCntStride] = tid == 0 ? (int32_t)qtot : (tid == kShards ? (int32_t)(qtot > qcap ? qtot - qcap : 0) : 0);
+        // min_Q of Q_r and the extractions of round r-1 as per-CTA values of round r-1
+        for (int i = tid; i < (int)gridDim.x; i += blockDim.x) {
+            p.cta_min[((r + 2) % 3) * kMaxCtas + i] = i == 0 ? minq : kInf;
+            p.cta_ext[((r + 2) % 3) * kMaxCtas + i] = i == 0 ? last_ext : 0;
+        }
+    }
+    if (tid == 0) {
+        s_small.on = 0;
+        ctrl->sm_end = end == 1;
+        ctrl->sm_r = r;
+        ctrl->sm_qtot = qtot;
+        ctrl->sm_theta_prev = theta_prev;
+        ctrl->sm_warm = warm;
+    }
+    __syncthreads();
+}
+
+#endif  // !SSSP_FUSE_UNIT
+
 // --------------------------------------------------------------------- the round loop
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned char* smem_raw = sssp_dyn_smem;
     WarpStage* stage = (WarpStage*)smem_raw;                                // [kWarps]
     uint64_t* s_keys = (uint64_t*)(smem_raw + kWarps * sizeof(WarpStage));  // [kSmemSamples]
     SelectSmem& sm = *(SelectSmem*)(s_keys + kSmemSamples);
@@ -1148,17 +1610,19 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     __shared__ int64_t cpref[kSeg + 1];  // segment prefix of the round's chunk list
     __shared__ uint64_t bc_u[3];         // min_Q (Delta / Dijkstra), CTA-0 theta, CTA-0 split
     __shared__ int64_t bc_dq;
+    __shared__ int32_t bc_ext;           // extractions of the previous round (small-round entry test)
     __shared__ int32_t bc_nl, bc_cnt;
     __shared__ int32_t tile_ctr[2];      // phase-A tile counters, by round parity
     __shared__ uint64_t red[kWarps];
     Ctrl* ctrl = p.ctrl;
     Warp W;
-    W.st = stage + (threadIdx.x >> 5);
-    W.fs = fstage + (threadIdx.x >> 5);
-    W.shard = (int)(warp_rank() % kShards);
+    W.init();
     W.qn = 0;
     W.fn = 0;
     W.pn = 0;
+#if !SSSP_FUSE_UNIT
+    if (lane_id() == 0) W.st()->ext = 0;
+#endif
     if (threadIdx.x == 0) tile_ctr[0] = tile_ctr[1] = 0;
     W.qdelta = 0;
 #if SSSP_PROF
@@ -1171,6 +1635,17 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     // the source in run ids (an isolated source of a compacted graph lies past p.n: it is
     // extracted in round 1 and relaxes nothing)
     const int32_t src = p.nofo ? p.nofo[p.source] : p.source;
+    // cold loop state of the small-frontier hand-over, kept in shared memory (not registers)
+    __shared__ struct {
+        int32_t epoch;    // small-frontier hand-backs seen
+        int32_t resumed;  // this round follows small rounds: qtot is CTA 0's count
+        int32_t cool;     // the last small attempt handed its first round back: the grid runs it
+        int32_t src_deg;  // round 1's frontier arcs
+    } ls;
+    if (threadIdx.x == 0) {
+        ls.epoch = ls.resumed = ls.cool = 0;
+        ls.src_deg = __ldg(p.off + src + 1) - __ldg(p.off + src);
+    }
     for (int64_t i = gtid; i < p.n; i += gsize) p.dist[i] = (i == src) ? 0ull : kInf;
     if (gtid == 0 && src >= p.n) p.dist[src] = 0;
     if (p.ext_count)
@@ -1179,6 +1654,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     for (int64_t i = gtid; i < 3 * kMaxCtas; i += gsize) {
         p.cta_min[i] = kInf;
         p.cta_delta[i] = 0;
+        p.cta_ext[i] = 0;
     }
     if (gtid == 0) {
         p.qbuf[1][0] = src;  // Q_1 lives in qbuf[1], shard 0
@@ -1188,7 +1664,12 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         ctrl->tot_extracted = ctrl->tot_edges = ctrl->tot_succ = ctrl->tot_inserts = 0;
         ctrl->tot_qscan = ctrl->max_q = ctrl->max_f = 0;
         ctrl->tot_dense = 0;
+        ctrl->sm_epoch = 0;
+        ctrl->sm_rounds = 0;
     }
+#if !SSSP_FUSE_UNIT
+    if (threadIdx.x == 0) s_small.on = 0;
+#endif
     grid_sync();
     if (gtid == 0) {
         p.counters[0] = 1;  // |Q_1| = 1 (slot 0, queue list, shard 0)
@@ -1203,6 +1684,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     uint64_t theta_prev = 0;
     int warm = 0;
     int64_t r = 1;
+    for (;;) {  // grid rounds, then small-frontier rounds while they apply, then grid rounds, ...
+    bool go_small = false;
     for (;; r++) {
         RoundCnt* C = &ctrl->cnt[r % 3];
         const Sharded<int32_t> QC = queue_of(p, r);
@@ -1210,6 +1693,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         // |Q_r| = |Q_{r-1}| + sum over CTAs of (inserts - extractions) in round r-1
         // warps 1 and 3, in parallel with warp 0's load_prefix: the previous round's |Q|
         // delta and min_Q delta (Delta* / Dijkstra)
+        if (small_on(FUSE) && (threadIdx.x >> 5) == 2) {
+            const int lane = lane_id();
+            const int32_t* ce = p.cta_ext + ((r + 2) % 3) * kMaxCtas;
+            int32_t se = 0;
+            for (int i = lane; i < (int)gridDim.x; i += 32) se += __ldcg(ce + i);
+            se = warp_sum(se);
+            if (lane == 0) bc_ext = se;
+        }
         if ((threadIdx.x >> 5) == 1 && r > 1) {
             const int lane = lane_id();
             const int64_t* cd = p.cta_delta + ((r + 2) % 3) * kMaxCtas;
@@ -1231,12 +1722,25 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             mn = warp_min_u64(mn);
             if (lane == 0) bc_u[0] = mn;
         }
+        W.set_round(queue_of(p, r + 1), C);  // (all warps are past the previous round's appends)
         load_prefix(QC, qpref);  // ends with __syncthreads
-        if (r > 1) qtot += bc_dq;
+        if (r > 1 && !ls.resumed) qtot += bc_dq;
         int64_t qn = qpref[kSeg];  // near part of Q_r
         if (qtot == 0) break;      // while |Q| > 0
         if (r > p.max_rounds) {
             if (gtid == 0) ctrl->status = SSSP_ERR_ROUNDS;
+            break;
+        }
+        // ---- small-frontier rounds: all of Q listed and at most kSmallQ ids -> CTA 0 runs the
+        // rounds alone (every CTA takes the same decision from the same counters)
+        const bool try_small = small_on(FUSE) && qtot == qn && qtot <= kSmallQ && bc_ext <= kSmallF && !ls.cool &&
+                               !(p.flags & SSSP_RUN_NO_SMALL) && (r > 1 || ls.src_deg <= kSmallArcs);
+        if (small_on(FUSE)) {
+            __syncthreads();  // (every thread has read ls)
+            if (threadIdx.x == 0) ls.resumed = ls.cool = 0;
+        }
+        if (try_small) {
+            go_small = true;
             break;
         }
         uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0, tn = 0;
@@ -1249,9 +1753,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         }
         if (threadIdx.x == 0) {
             p.cta_delta[((r + 1) % 3) * kMaxCtas + blockIdx.x] = 0;
+            p.cta_ext[((r + 1) % 3) * kMaxCtas + blockIdx.x] = 0;
         }
-        W.qnext = queue_of(p, r + 1);
-        W.C = C;
 
         // ---- ExtDist (Table tab:framework) and near/far maintenance
         uint64_t theta;
@@ -1429,7 +1932,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         const bool phase_b_work = cpref[kSeg] + nl > 0;
         if (phase_b_work) {
             const uint64_t tb = STATS ? globaltimer() : 0;
-            phase_b<POL, STATS, FUSE, BIDIR>(p, CL, cpref, nl, W);
+            phase_b<POL, STATS, FUSE, BIDIR>(p, CL, cpref, nl, W, warp_rank(), ((int64_t)gridDim.x * blockDim.x) >> 5);
             if (STATS && lane_id() == 0) atomicAdd(&C->busy_b, (unsigned long long)(globaltimer() - tb));
         }
         drain_pending<POL, STATS, FUSE, BIDIR>(p, W);  // deferred WriteMins count in min_Q
@@ -1477,6 +1980,62 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
             ctrl->max_q = qtot > ctrl->max_q ? qtot : ctrl->max_q;
             ctrl->max_f = f > ctrl->max_f ? f : ctrl->max_f;
         }
+    }
+        if (!small_on(FUSE) || !go_small) break;
+#if !SSSP_FUSE_UNIT
+        if constexpr (small_on(FUSE)) {
+        // ---- small-frontier rounds (outside the grid's round loop: no call or cold state
+        // inside its register allocation)
+        const Sharded<int32_t> QC = queue_of(p, r);
+        const int32_t epoch = ls.epoch + 1;
+        if (blockIdx.x == 0) {
+            uint64_t minq = 0;
+            if (uses_min(POL)) {
+                if (threadIdx.x < 32) {
+                    const uint64_t* cm = p.cta_min + ((r + 2) % 3) * kMaxCtas;
+                    uint64_t mn = kInf;
+                    for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) {
+                        const uint64_t x = __ldcg((const unsigned long long*)(cm + i));
+                        mn = x < mn ? x : mn;
+                    }
+                    mn = warp_min_u64(mn);
+                    if (threadIdx.x == 0) bc_u[0] = mn;
+                }
+                __syncthreads();
+                minq = bc_u[0];
+            }
+            small_rounds<POL, STATS, FUSE, BIDIR>(p, r, qtot, theta_prev, warm, minq, QC, qpref, cpref, red);
+            if (threadIdx.x == 0) {
+                __threadfence();
+                st_release_i32(&ctrl->sm_epoch, epoch);
+                ls.epoch = epoch;
+            }
+        } else {
+            if (threadIdx.x == 0)
+                while (ld_acquire_i32(&ctrl->sm_epoch) < epoch) __nanosleep(128);
+            if (threadIdx.x == 0) ls.epoch = epoch;
+            __syncthreads();
+        }
+        const int64_t r_new = ld_volatile_i64(&ctrl->sm_r);
+        const bool over = ld_volatile_i32(&ctrl->sm_end) != 0;
+        qtot = ld_volatile_i64(&ctrl->sm_qtot);
+        theta_prev = ld_volatile_u64(&ctrl->sm_theta_prev);
+        warm = ld_volatile_i32(&ctrl->sm_warm);
+        split = kInf;  // small rounds list all of Q
+        if (threadIdx.x == 0) {
+            tile_ctr[0] = tile_ctr[1] = 0;
+            p.cta_delta[(r_new % 3) * kMaxCtas + blockIdx.x] = 0;
+            p.cta_ext[(r_new % 3) * kMaxCtas + blockIdx.x] = 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            ls.cool = r_new == r;  // the first small round was too large: the grid runs it
+            ls.resumed = 1;
+        }
+        r = r_new;
+        if (over) break;
+        }
+#endif
     }
     if (gtid == 0) ctrl->rounds = r - 1;
     // S6 output: strip the flag bit (every reached vertex was extracted; INF stays INF)

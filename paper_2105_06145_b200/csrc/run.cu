@@ -101,6 +101,7 @@ struct Layout {
     int32_t* counters;
     uint64_t* cta_min;
     int64_t* cta_delta;
+    int32_t* cta_ext;
     Desc* light;
     uint64_t* samples;
     Ctrl* ctrl;
@@ -136,6 +137,7 @@ Layout carve(void* base, int32_t n, int64_t m, uint32_t flags) {
     L.counters = c.take<int32_t>((size_t)3 * 2 * kSeg * kCntStride);
     L.cta_min = c.take<uint64_t>((size_t)3 * kMaxCtas);
     L.cta_delta = c.take<int64_t>((size_t)3 * kMaxCtas);
+    L.cta_ext = c.take<int32_t>((size_t)3 * kMaxCtas);
     L.dist = c.take<uint64_t>(n);
     L.dist2 = c.take<uint64_t>(n);
     L.q0 = c.take<int32_t>(qlen);
@@ -339,6 +341,7 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
     b.counters = L.counters;
     b.cta_min = L.cta_min;
     b.cta_delta = L.cta_delta;
+    b.cta_ext = L.cta_ext;
     b.light = L.light;
     b.samples = L.samples;
     b.ctrl = L.ctrl;

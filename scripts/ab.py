@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--config", default="rmat24")
     ap.add_argument("--cases", default="rho:262144")
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--kw", default="", help="run options, e.g. fuse_budget=16,small=0")
     a = ap.parse_args()
     import torch
     import gen
@@ -37,16 +38,17 @@ def main():
     hs = [m.SSSP.from_graph(g) for m in mods]
     d = torch.empty(g.n, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    kw = {k: int(v) for k, v in (x.split("=") for x in a.kw.split(",") if x)}
     for case in a.cases.split(","):
         pol, par = case.split(":")
         par = int(par)
         ts = [[] for _ in libs]
         for h in hs:
-            h.run(g.source, pol, par, out=d)
+            h.run(g.source, pol, par, out=d, **kw)
         for r in range(a.reps):
             for i, h in enumerate(hs):
                 flush.zero_()
-                h.run(g.source, pol, par, out=d, seed=r)
+                h.run(g.source, pol, par, out=d, seed=r, **kw)
                 ts[i].append(h.last_stats["kernel_ms"])
         med = [statistics.median(t) for t in ts]
         print(f"{a.config} {pol}:{par} " + "  ".join(f"{l}={m:.3f}ms" for l, m in zip(libs, med))
