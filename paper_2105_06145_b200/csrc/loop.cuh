@@ -319,6 +319,7 @@ constexpr int kPend = 64;  // deferred WriteMins: pending WriteMins per warp (dr
 struct WarpStage {
 #if !SSSP_FUSE_UNIT
     int32_t ext;          // vertices this warp extracted this round (lane 0 counts; small-round entry test)
+    int32_t snxt;         // small rounds: which s_small.q[] this warp appends Q_{r+1} to
 #endif
     int32_t take[kTBuf];  // ids that pass the theta test, extracted 32 at a time
     int32_t q[kQBuf];     // ids appended to the next queue
@@ -358,12 +359,13 @@ struct SmallSmem {
     int32_t q[2][kSmallQ];     // Q_r / Q_{r+1} ids (entries >= kSmallQ of Q_{r+1} go to gq)
     int32_t qcnt[2];
     int32_t on;                // 1 while CTA 0 runs small rounds: wq_flush appends here
-    int32_t nxt;               // which q[] receives Q_{r+1}
-    int32_t* gq;               // Q_{r+1} in the grid's flat layout (overflow, and the hand-back)
+    int32_t* gq[2];            // q[k]'s continuation in the grid's flat layout (overflow, hand-back)
     int64_t qcap;
-    unsigned long long arcs;   // arcs of the round's frontier
-    int32_t heavy;             // a vertex of degree > kLight was extracted (chunk list in use)
-    int32_t ext;               // vertices extracted this round (fusion included)
+    // per-round scalars, by round parity (a round resets its own before its first barrier
+    // while the previous round's may still be read: no barrier between rounds)
+    unsigned long long arcs[2];  // arcs of the round's frontier
+    int32_t heavy[2];            // a vertex of degree > kLight was extracted (chunk list in use)
+    int32_t ext[2];              // vertices extracted this round (fusion included)
 };
 #if !SSSP_FUSE_UNIT
 __shared__ SmallSmem s_small;
@@ -518,15 +520,16 @@ __device__ __forceinline__ void wq_flush(Warp& W) {
 #if !SSSP_FUSE_UNIT
     if (s_small.on) {  // small-frontier rounds (CTA 0 alone): Q_{r+1} in shared memory
         int32_t pos = 0;
-        if (lane_id() == 0) pos = atomicAdd(&s_small.qcnt[s_small.nxt], W.qn);
+        const int nx = W.st()->snxt;
+        if (lane_id() == 0) pos = atomicAdd(&s_small.qcnt[nx], W.qn);
         pos = __shfl_sync(kFull, pos, 0);
-        int32_t* sq = s_small.q[s_small.nxt];
+        int32_t* sq = s_small.q[nx];
         for (int32_t i = lane_id(); i < W.qn; i += 32) {
             const int32_t v = W.st()->q[i], j = pos + i;
             if (j < kSmallQ)
                 sq[j] = v;
             else
-                *flat_slot(s_small.gq, s_small.qcap, j) = v;
+                *flat_slot(s_small.gq[nx], s_small.qcap, j) = v;
         }
         __syncwarp();
         W.qn = 0;
@@ -1334,10 +1337,18 @@ __device__ __forceinline__ void small_rounds(const RunParams& p, int64_t r, int6
         const int sg = seg_of(qpref0, i);
         s_small.q[0][i] = ld_cg_i32(QC0.seg(sg) + (i - qpref0[sg]));
     }
-    if (tid == 0) {
+    if (tid == 0) {  // (q[k] is Q of the rounds r0 + k, r0 + k + 2, ...)
         s_small.on = 1;
         s_small.qcnt[0] = (int32_t)qtot;
+        s_small.qcnt[1] = 0;
         s_small.qcap = qcap;
+        s_small.gq[0] = p.qbuf[r & 1];
+        s_small.gq[1] = p.qbuf[(r + 1) & 1];
+        for (int k = 0; k < 2; k++) {
+            s_small.arcs[k] = 0;
+            s_small.heavy[k] = 0;
+            s_small.ext[k] = 0;
+        }
     }
     W.split = kInf;
     W.fuse_theta = 0;
@@ -1395,18 +1406,10 @@ __device__ __forceinline__ void small_rounds(const RunParams& p, int64_t r, int6
         const int nxt = cur ^ 1;
         if (tid < 2 * kSeg)  // counters of slot (r+1)%3 (the chunk list of round r+1)
             p.counters[((int64_t)(((r + 1) % 3) * 2) * kSeg + tid) * kCntStride] = 0;
-        if (tid == 0) {
-            reset_cnt(&ctrl->cnt[(r + 1) % 3]);
-            s_small.qcnt[nxt] = 0;
-            s_small.nxt = nxt;
-            s_small.gq = p.qbuf[(r + 1) & 1];
-            s_small.arcs = 0;
-            s_small.heavy = 0;
-            s_small.ext = 0;
-        }
-        W.set_round(s_rnd.qnext, C);  // (C: thread 0, before the barrier below)
+        if (tid == 0) reset_cnt(&ctrl->cnt[(r + 1) % 3]);
+        if (lane == 0) W.st()->snxt = nxt;
         W.fuse_theta = (FUSE && !snap) ? theta : 0;
-        __syncthreads();
+        // (no barrier: every shared scalar this round uses was reset during the previous one)
         // ---- Extract(theta): delete every queued id, keep those above theta
         int32_t id[kE], beg[kE], deg[kE];
         uint64_t d[kE];
@@ -1443,9 +1446,9 @@ __device__ __forceinline__ void small_rounds(const RunParams& p, int64_t r, int6
             }
         }
         arcs = warp_sum(arcs);
-        if (lane == 0 && arcs) atomicAdd(&s_small.arcs, arcs);
+        if (lane == 0 && arcs) atomicAdd(&s_small.arcs[r & 1], arcs);
         __syncthreads();
-        if (s_small.arcs > (unsigned long long)kSmallArcs) {
+        if (s_small.arcs[r & 1] > (unsigned long long)kSmallArcs) {
             // too much work for one SM: undo the deletions and hand round r to the grid
 #pragma unroll
             for (int e = 0; e < kE; e++)
@@ -1454,6 +1457,12 @@ __device__ __forceinline__ void small_rounds(const RunParams& p, int64_t r, int6
             warm = warm0;
             end = 2;
             break;
+        }
+        if (tid == 0) {  // the next round's scalars (q[cur] is read no more this round)
+            s_small.qcnt[cur] = 0;
+            s_small.arcs[(r + 1) & 1] = 0;
+            s_small.heavy[(r + 1) & 1] = 0;
+            s_small.ext[(r + 1) & 1] = 0;
         }
         // kept ids go to Q_{r+1} first (in queue order)
 #pragma unroll
@@ -1484,7 +1493,7 @@ __device__ __forceinline__ void small_rounds(const RunParams& p, int64_t r, int6
             const bool heavy = deg[e] > kLight;
             const bool light = id[e] >= 0 && deg[e] > 0 && !heavy;
             if (__any_sync(kFull, heavy)) {
-                if (lane == 0) s_small.heavy = 1;
+                if (lane == 0) s_small.heavy[r & 1] = 1;
                 emit_chunks(CL, W.shard(), heavy, d[e], beg[e], deg[e], C, STATS);
             }
             if (__any_sync(kFull, light))
@@ -1492,7 +1501,7 @@ __device__ __forceinline__ void small_rounds(const RunParams& p, int64_t r, int6
         }
         fuse_drain<POL, STATS, FUSE, BIDIR>(p, W);
         __syncthreads();
-        if (s_small.heavy) {  // heavy vertices: all warps of the CTA stride over their chunks
+        if (s_small.heavy[r & 1]) {  // heavy vertices: all warps of the CTA stride over their chunks
             load_prefix(CL, cpref);
             phase_b<POL, STATS, FUSE, BIDIR>(p, CL, cpref, 0, W, wid, kWarps);
         }
@@ -1517,14 +1526,15 @@ __device__ __forceinline__ void small_rounds(const RunParams& p, int64_t r, int6
         }
         W.qdelta = 0;
         if (lane == 0 && W.st()->ext) {
-            atomicAdd(&s_small.ext, W.st()->ext);
+            atomicAdd(&s_small.ext[r & 1], W.st()->ext);
             W.st()->ext = 0;
         }
         __syncthreads();
-        const int32_t ext = s_small.ext;
+        const int32_t ext = s_small.ext[r & 1];
         if (uses_min(POL)) {
             uint64_t mn = kInf;
-            for (int i = 0; i < kWarps; i++) mn = red[i] < mn ? red[i] : mn;
+            static_assert(kWarps == 32, "one per-warp minimum per lane");
+            mn = warp_min_u64(red[lane]);  // every warp reduces the 32 warp minima itself
             minq = mn;
         }
         const int64_t qnext = s_small.qcnt[nxt];
@@ -1568,7 +1578,6 @@ __device__ __forceinline__ void small_rounds(const RunParams& p, int64_t r, int6
             end = 2;
             break;
         }
-        __syncthreads();  // (the next round reuses the other queue buffer and s_small fields)
     }
     // ---- hand back: Q_r in the grid's layout (flat: shard-0 segment, then the spill segment)
     if (end == 2) {
