@@ -15,7 +15,7 @@ namespace sssp {
 
 KernelUnit SSSP_UNIT_NAME(kernel_unit, INST_POL, INST_BIDIR, INST_FUSE)() {
     constexpr bool B = INST_BIDIR != 0, F = INST_FUSE != 0;
-    return KernelUnit{sssp_round_loop<INST_POL, false, F, B>, sssp_round_loop<INST_POL, true, F, B>, smem_bytes(F)};
+    return KernelUnit{sssp_round_loop<INST_POL, false, F, B>, sssp_round_loop<INST_POL, true, F, B>, smem_bytes(F), kBlock};
 }
 
 }  // namespace sssp

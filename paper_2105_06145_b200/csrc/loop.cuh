@@ -86,7 +86,7 @@ constexpr int kWarps = kBlock / 32;
 #define SSSP_FUSE 64
 #endif
 constexpr int kEnt = 2;                      // queue entries per lane per Extract step (large queues)
-constexpr int kQBuf = 256;                   // staged queue ids per warp (>= 32 * kArcs)
+constexpr int kQBuf = 32 * kArcs > 256 ? 32 * kArcs : 256;  // staged queue ids per warp (>= 32 * kArcs)
 constexpr int kTBuf = 32 * kEnt + 32;        // staged extracted ids per warp
 constexpr int kFBuf = 32 * kArcs + 64;       // fused vertices waiting for their relax, per warp
 constexpr int kFuseBudget = SSSP_FUSE;       // fused vertices per warp per round (0 = off)
@@ -686,10 +686,11 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
         cnt += out[t] == kAppend;
         fcnt += out[t] == kFused;
     }
-    static_assert(kArcs < 8, "3-bit per-lane counts");
+    constexpr int kCntBits = kArcs < 8 ? 3 : (kArcs < 16 ? 4 : 5);  // per-lane count bits
+    static_assert(kArcs < 32, "per-lane counts");
     if (__any_sync(kFull, cnt != 0)) {
         int32_t tot;
-        const int32_t excl = warp_excl_scan_small<3>(cnt, tot);
+        const int32_t excl = warp_excl_scan_small<kCntBits>(cnt, tot);
         if (W.qn + tot > kQBuf) wq_flush(W);
         int32_t pos = W.qn + excl;
 #pragma unroll
@@ -699,7 +700,7 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
     }
     if (FUSE && fuse && __any_sync(kFull, fcnt != 0)) {
         int32_t tot;
-        const int32_t excl = warp_excl_scan_small<3>(fcnt, tot);
+        const int32_t excl = warp_excl_scan_small<kCntBits>(fcnt, tot);
         int32_t pos = W.fn + excl;
 #pragma unroll
         for (int t = 0; t < kArcs; t++)
@@ -1533,8 +1534,8 @@ __device__ __forceinline__ void small_rounds(const RunParams& p, int64_t r, int6
         const int32_t ext = s_small.ext[r & 1];
         if (uses_min(POL)) {
             uint64_t mn = kInf;
-            static_assert(kWarps == 32, "one per-warp minimum per lane");
-            mn = warp_min_u64(red[lane]);  // every warp reduces the 32 warp minima itself
+            static_assert(kWarps <= 32, "one per-warp minimum per lane");
+            mn = warp_min_u64(lane < kWarps ? red[lane] : kInf);  // every warp reduces the warp minima itself
             minq = mn;
         }
         const int64_t qnext = s_small.qcnt[nxt];
@@ -1611,10 +1612,8 @@ __device__ __forceinline__ void small_rounds(const RunParams& p, int64_t r, int6
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams p) {
     unsigned char* smem_raw = sssp_dyn_smem;
-    WarpStage* stage = (WarpStage*)smem_raw;                                // [kWarps]
     uint64_t* s_keys = (uint64_t*)(smem_raw + kWarps * sizeof(WarpStage));  // [kSmemSamples]
     SelectSmem& sm = *(SelectSmem*)(s_keys + kSmemSamples);
-    FuseStage* fstage = (FuseStage*)(smem_raw + kSmemBase);                  // [kWarps], FUSE only
     __shared__ int64_t qpref[kSeg + 1];  // segment prefix of Q_r's near part
     __shared__ int64_t cpref[kSeg + 1];  // segment prefix of the round's chunk list
     __shared__ uint64_t bc_u[3];         // min_Q (Delta / Dijkstra), CTA-0 theta, CTA-0 split
@@ -2085,6 +2084,7 @@ static constexpr size_t smem_bytes(bool fuse) { return kSmemBase + (fuse ? kWarp
 struct KernelUnit {
     KernelFn plain, stats;
     size_t smem;
+    int block;  // threads per CTA of this unit's kernels (SSSP_BLOCK may be unit-specific, build.py)
 };
 #define SSSP_DECLARE_UNIT(P, B, F) KernelUnit kernel_unit_##P##_##B##_##F();
 #define SSSP_DECLARE_UNITS(P) \

@@ -70,6 +70,7 @@ struct sssp_handle {
     cudaEvent_t ev[2];
     int num_sms;
     int grid[5][2][4];
+    int last_block;  // threads per CTA of the last launch (unit-specific)
     // batch runs: a copy stream overlaps the read-back of run i with run i+1
     cudaStream_t copy_stream;
     cudaEvent_t ev_done[2], ev_copied[2];
@@ -167,7 +168,7 @@ KernelUnit unit_for(int pol, int mode) {
         SSSP_UNIT_CASE(4)
     }
 #undef SSSP_UNIT_CASE
-    return KernelUnit{nullptr, nullptr, 0};
+    return KernelUnit{nullptr, nullptr, 0, 0};
 }
 KernelFn kernel_for(int pol, bool stats, int mode) {
     const KernelUnit u = unit_for(pol, mode);
@@ -218,9 +219,10 @@ sssp_status launch_run(sssp_handle* h, int32_t source, sssp_policy policy, uint6
     const int grid = h->grid[policy][st][mode];
     void* args[] = {&p};
     cudaError_t e =
-        cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kBlock), args, unit_for(policy, mode).smem, h->stream);
+        cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(unit_for(policy, mode).block), args, unit_for(policy, mode).smem, h->stream);
     if (e != cudaSuccess) return cuda_error(e, "round-loop launch");
     *grid_out = grid;
+    h->last_block = unit_for(policy, mode).block;
     *max_rounds_out = p.max_rounds;
     return SSSP_OK;
 }
@@ -354,7 +356,7 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t* d_offsets, const in
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 if (e == cudaSuccess)
                     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kernel_for(pol, st, sn),
-                                                                      kBlock, smem);
+                                                                      unit_for(pol, sn).block, smem);
                 if (e != cudaSuccess || per_sm < 1) {
                     sssp_destroy(h);
                     return e != cudaSuccess ? cuda_error(e, "occupancy query")
@@ -434,7 +436,7 @@ sssp_status sssp_run_ex(sssp_handle* h, int32_t source, sssp_policy policy, uint
         stats->max_frontier = c->max_f;
         stats->dense_scanned = c->tot_dense;
         stats->grid_blocks = grid;
-        stats->block_threads = kBlock;
+        stats->block_threads = h->last_block;
         float ms = 0.f;
         cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]);
         stats->kernel_ms = ms;
@@ -498,7 +500,7 @@ sssp_status sssp_run_batch_host(sssp_handle* h, const int32_t* h_sources, int32_
         memset(stats, 0, sizeof(*stats));
         stats->rounds = rounds;
         stats->grid_blocks = grid;
-        stats->block_threads = kBlock;
+        stats->block_threads = h->last_block;
         float ms = 0.f;
         cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]);
         stats->kernel_ms = ms;  // whole batch, read-backs included

@@ -25,7 +25,13 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--out", default="gpurun_out/param_study.jsonl")
     ap.add_argument("--md", default="gpurun_out/param_study.md")
+    ap.add_argument("--traces", default=None, help="also record per-step traces of rho / Delta* / BF (jsonl)")
+    ap.add_argument("--trace-configs", default="rmat24,rgg4m,grid4096")
+    ap.add_argument("--from-jsonl", action="store_true", help="only rewrite --md from --out (and --traces)")
     args = ap.parse_args()
+    if args.from_jsonl:
+        write_md([json.loads(ln) for ln in open(args.out)], args.md, args.traces)
+        return
     import torch
 
     import gen
@@ -53,16 +59,85 @@ def main():
                    "rounds": statistics.median(rs), "edges_per_m": st["edges"] / g.m}
             recs.append(rec)
             print(json.dumps(rec), flush=True)
+        if args.traces and name in args.trace_configs.split(","):
+            # visited vertices per step (paper Fig. visted-per-step) at the best rho / Delta*
+            mine = [r for r in recs if r["config"] == name]
+            for pol in ("rho", "delta", "bellman_ford"):
+                b = min((r for r in mine if r["policy"] == pol), key=lambda r: r["ms"])
+                _, st, tr, _ = h.run(g.source, pol, b["param"], out=d, stats=True, trace_cap=1 << 20,
+                                     max_rounds=300000)
+                with open(args.traces, "a") as f:
+                    f.write(json.dumps({"config": name, "n": g.n, "m": g.m, "policy": pol, "param": b["param"],
+                                        "ms": b["ms"], "fsize": tr["fsize"].tolist(), "edges": tr["edges"].tolist(),
+                                        "qsize": tr["qsize"].tolist(), "fused": tr["fused"].tolist()}) + "\n")
         h.close()
     with open(args.out, "w") as f:
         for r in recs:
             f.write(json.dumps(r) + "\n")
-    write_md(recs, args.md)
+    write_md(recs, args.md, args.traces)
 
 
-def write_md(recs, path):
+def fixed_rho(recs):
+    """One rho for every config (the paper's PQ-rho-fix): the rho of the sweep
+    with the smallest geometric-mean slowdown against each config's best rho."""
+    import math
+
+    rho = [r for r in recs if r["policy"] == "rho"]
+    cfgs = list(dict.fromkeys(r["config"] for r in rho))
+    best = {c: min((r for r in rho if r["config"] == c), key=lambda r: r["ms"]) for c in cfgs}
+    rows = []
+    for p in sorted(set(r["param"] for r in rho)):
+        at = {c: next((r for r in rho if r["config"] == c and r["param"] == p), None) for c in cfgs}
+        if any(v is None for v in at.values()):
+            continue
+        loss = {c: at[c]["ms"] / best[c]["ms"] for c in cfgs}
+        geo = math.exp(sum(math.log(x) for x in loss.values()) / len(loss))
+        rows.append((geo, max(loss.values()), p, loss))
+    rows.sort(key=lambda t: t[0])
+    return cfgs, best, rows
+
+
+def step_table(t, bins=20):
+    """Visited vertices (|F_r|, fusion included) and arcs per step; long runs grouped into bins."""
+    f, e, q = t["fsize"], t["edges"], t["qsize"]
+    R = len(f)
+    out = [f"### {t['config']} {t['policy']}" + ("" if t["policy"] == "bellman_ford" else
+                                                 f" 2^{t['param'].bit_length() - 1}") +
+           f" ({R} steps, {t['ms']:.3f} ms; visited / n = {sum(f) / t['n']:.2f}, arcs / m = {sum(e) / t['m']:.2f})", ""]
+    if R <= 40:
+        out += ["| step | \\|Q\\| | visited \\|F\\| | arcs |", "|---|---|---|---|"]
+        out += [f"| {i + 1} | {q[i]:,} | {f[i]:,} | {e[i]:,} |" for i in range(R)]
+    else:
+        k = (R + bins - 1) // bins
+        out += ["| steps | mean \\|Q\\| | visited (sum) | visited (max step) | arcs (sum) |", "|---|---|---|---|---|"]
+        for s in range(0, R, k):
+            sl = slice(s, min(R, s + k))
+            out.append(f"| {s + 1}-{min(R, s + k)} | {sum(q[sl]) / len(q[sl]):,.0f} | {sum(f[sl]):,} | "
+                       f"{max(f[sl]):,} | {sum(e[sl]):,} |")
+    return out + [""]
+
+
+def write_md(recs, path, traces=None):
     out = ["# Parameter study (SURVEY f-3), B200, one source per config (the workload source)", "",
            "Median device time of `sssp_run` over 3 runs (L2 flushed before each), default live rounds.", ""]
+    cfgs, best, rows = fixed_rho(recs)
+    if rows:
+        geo, mx, p, loss = rows[0]
+        out += [f"## One fixed GPU rho for all configs (PQ-rho-fix analogue, P:1575, P:1601)", "",
+                f"rho = 2^{p.bit_length() - 1} has the smallest geometric-mean slowdown against each config's best "
+                f"rho ({geo:.3f}x; worst {mx:.2f}x). Candidates ranked:", "",
+                "| rho | geo-mean loss | worst | " + " | ".join(cfgs) + " |", "|---|---|---|" + "---|" * len(cfgs)]
+        for geo_, mx_, p_, loss_ in rows[:6]:
+            out.append(f"| 2^{p_.bit_length() - 1} | {geo_:.3f} | {mx_:.2f} | " +
+                       " | ".join(f"{loss_[c]:.2f}" for c in cfgs) + " |")
+        out += ["", "Best rho per config: " + ", ".join(f"{c} 2^{best[c]['param'].bit_length() - 1} "
+                                                        f"({best[c]['ms']:.3f} ms)" for c in cfgs) + ".", ""]
+    if traces and os.path.exists(traces):
+        out += ["## Visited vertices per step (paper Fig. visted-per-step, P:1653-1678)", "",
+                "From the trace rows of a stats run at each policy's best parameter. Visited = |F_r|, the vertices "
+                "extracted in step r (vertices relaxed on the spot by fusion included).", ""]
+        for ln in open(traces):
+            out += step_table(json.loads(ln))
     for name in dict.fromkeys(r["config"] for r in recs):
         rs = [r for r in recs if r["config"] == name]
         out += [f"## {name}", "", "| policy | param | ms | GTEPS | rounds | arcs scanned / m |", "|---|---|---|---|---|---|"]

@@ -157,6 +157,36 @@ def test_errors(cuda_device):
         assert e.value.status == P.SSSP_ERR_INVALID_GRAPH
 
 
+def test_create_failure_loop_releases(cuda_device):
+    """sssp_create's failure paths release the handle's stream and events (sssp_destroy on
+    every error return): 200 rejected creates leave device memory where it was and a valid
+    handle still works afterwards."""
+    import torch
+
+    P = _P()
+    g = gen.make("grid64")
+    off = torch.tensor(g.offsets, device="cuda")
+    idx = torch.tensor(g.indices, device="cuda")
+    w = torch.tensor(g.weights.view(np.int32), device="cuda")
+    w[5] = 0
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(200):
+        with pytest.raises(P.SSSPError) as e:
+            P.SSSP(off, idx, w, validate=True)
+        assert e.value.status == P.SSSP_ERR_INVALID_GRAPH
+    torch.cuda.synchronize()
+    import gc
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < (64 << 20), f"device memory dropped by {(free0 - free1) >> 20} MiB over 200 failed creates"
+    h = P.SSSP.from_graph(g)
+    _assert_same(P.dist_to_u64(h.run(g.source, "delta", 4096)), oracle.dijkstra(g), "after failed creates")
+    h.close()
+
+
 TRACE_FIELDS = ["qsize", "fsize", "edges", "inserts", "theta"]
 
 
@@ -216,6 +246,31 @@ def test_sampled_rho_invariants(cuda_device):
             # |Q| <= rho rounds drain the queue (theta = INF)
             small = q <= rho
             assert (tr["theta"][small] == INF).all() and (tr["fsize"][small] == q[small]).all()
+
+
+@pytest.mark.parametrize("name,rhos", [("rmat20", (1 << 12, 1 << 15)), ("rgg1m", (1 << 10, 1 << 13))])
+def test_in_loop_theta_quality(cuda_device, name, rhos):
+    """The in-loop sampled theta_r lands near the rho-th smallest key of Q_r (App. cpam,
+    P:1928-1933: rank within [rho/2, 2 rho] w.h.p.).  In snapshot rounds Extract deletes
+    exactly the keys <= theta_r before any relax, so |F_r| = #{v in Q_r : delta[v] <= theta_r}
+    = rank(theta_r); with near/far on, the near part holds Q's rho smallest keys (R18), so the
+    rank is over all of Q either way.  Warm-up off (rho_eff = rho in every round)."""
+    P = _P()
+    g = gen.make(name)
+    d_ref = oracle.dijkstra(g)
+    h = P.SSSP.from_graph(g)
+    for rho in rhos:
+        for nearfar in (True, False):
+            for seed in range(2):
+                d, st, tr, _ = h.run(g.source, "rho", rho, seed=seed, trace_cap=1 << 16, snapshot=True,
+                                     warmup=False, nearfar=nearfar)
+                _assert_same(P.dist_to_u64(d), d_ref, f"{name}/rho{rho}/nf{nearfar}/seed{seed}")
+                big = tr["qsize"] > rho  # rounds that sample (|Q| <= rho drains, P:1376)
+                f = tr["fsize"][big]
+                assert len(f) >= 3, f"{name}/rho{rho}: only {len(f)} sampled rounds"
+                ok = (f >= rho // 2) & (f <= 2 * rho)
+                assert ok.mean() >= 0.95, (f"{name}/rho{rho}/nf{nearfar}/seed{seed}: rank(theta_r) in [rho/2, 2rho] "
+                                           f"in {ok.sum()}/{len(f)} rounds; ranks {f[~ok][:10]}")
 
 
 def test_determinism_and_run_host(cuda_device):
