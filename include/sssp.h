@@ -240,7 +240,10 @@ sssp_status sssp_pq_update(sssp_pq *q, const int32_t *d_ids, int64_t count);
  * theta to d_out[0..*h_count) in unspecified order and deletes them from Q.
  * Exclusive with other calls (stream order).  Synchronous: *h_count is host
  * memory.  If more than cap ids qualify: SSSP_ERR_CAPACITY, *h_count = the
- * number that qualify, and Q is unchanged. */
+ * number that qualify, and Q is unchanged.  A range error latched by an earlier
+ * update is reported by this call after the extract has run (*h_count valid).
+ * One launch (two if cap < n: the qualifying ids are counted first) and one
+ * synchronisation. */
 sssp_status sssp_pq_extract(sssp_pq *q, uint64_t theta, int32_t *d_out, int64_t cap, int64_t *h_count);
 
 /* |Q| (synchronous). */

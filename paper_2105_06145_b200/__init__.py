@@ -281,10 +281,14 @@ class LabPQ:
         self._last_ids = ids  # keep alive until the stream consumes it
         _check(sssp_pq_update(self._q, _ptr(ids), ids.numel()), "sssp_pq_update")
 
-    def extract(self, theta, cap=None):
+    def extract(self, theta, cap=None, out=None):
         torch = _torch()
         cap = self.n if cap is None else cap
-        out = torch.empty(max(cap, 1), dtype=torch.int32, device=self.keys.device)
+        if out is None:
+            out = torch.empty(max(cap, 1), dtype=torch.int32, device=self.keys.device)
+        elif not (out.device == self.keys.device and out.dtype == torch.int32 and out.is_contiguous()
+                  and out.numel() >= max(cap, 1)):
+            raise ValueError(f"out must be a contiguous int32 tensor of >= {max(cap, 1)} elements on {self.keys.device}")
         cnt = ctypes.c_int64(0)
         _check(sssp_pq_extract(self._q, int(theta), _ptr(out), cap, ctypes.byref(cnt)), "sssp_pq_extract")
         return out[: cnt.value]
@@ -305,9 +309,13 @@ class LabPQ:
         _check(sssp_pq_reduce_min(self._q, ctypes.byref(t)), "sssp_pq_reduce_min")
         return int(t.value)
 
-    def queue(self):
+    def queue(self, out=None):
         torch = _torch()
-        out = torch.empty(max(self.n, 1), dtype=torch.int32, device=self.keys.device)
+        if out is None:
+            out = torch.empty(max(self.n, 1), dtype=torch.int32, device=self.keys.device)
+        elif not (out.device == self.keys.device and out.dtype == torch.int32 and out.is_contiguous()
+                  and out.numel() >= max(self.n, 1)):
+            raise ValueError(f"out must be a contiguous int32 tensor of >= {max(self.n, 1)} elements on {self.keys.device}")
         cnt = ctypes.c_int64(0)
         _check(sssp_pq_queue(self._q, _ptr(out), self.n, ctypes.byref(cnt)), "sssp_pq_queue")
         return out[: cnt.value]

@@ -2,8 +2,10 @@
 """Standalone LaB-PQ (sssp_pq_*) timings on one GPU (exploration; profiles/pq_bench_r1.md).
 
 n = 2^24 keys (uniform random 40-bit), batches of random ids (with duplicates).  Each call
-is timed with CUDA events around the binding call; calls that return a host value
-(extract count, size, theta, min) include their synchronisation.
+is timed with CUDA events around the binding call (output tensors allocated beforehand);
+calls that return a host value (extract count, size, theta, min) include their
+synchronisation.  Device time per call: run under
+`ncu --metrics gpu__time_duration.sum --csv` and sum the kernels of each call (scripts/pq_ncu.py).
 """
 import os
 import statistics
@@ -50,9 +52,10 @@ for mode in (False, True):
 ms, mn = timed(lambda: pq.reduce_min())
 print(f"reduce_min: {ms * 1e3:9.1f} us", flush=True)
 th = pq.select(1 << 18, seed=3, exact=True)
-ms, got = timed(lambda: pq.extract(th, cap=n), reps=1)  # mutates Q: one timed call
+outbuf = torch.empty(n, dtype=torch.int32, device="cuda")
+ms, got = timed(lambda: pq.extract(th, cap=n, out=outbuf), reps=1)  # mutates Q: one timed call
 print(f"extract theta = rho-th key: {ms * 1e3:9.1f} us, {got.numel():,} ids "
       f"(|Q| {sz:,} scanned: {sz / ms / 1e6:.2f} G ids/s)", flush=True)
-ms, q = timed(lambda: pq.queue(), reps=3)
+ms, q = timed(lambda: pq.queue(out=outbuf), reps=3)
 print(f"queue   ({q.numel():,} ids): {ms * 1e3:9.1f} us", flush=True)
 pq.close()
