@@ -33,7 +33,10 @@ POLICIES = 5  # SSSP_RHO .. SSSP_DELTA_STEPPING (include/sssp.h)
 # With deferred WriteMins the rho unit does best at 5 arcs per lane (A/B against 6:
 # rmat24 rho = 2^18 -2.9 %, 2^17 -3.1 %, rmat20 -4 %; 7 arcs: +2 %).
 # The Delta* unit likewise (rmat24 -1.6 %, rmat20 -2.4 %); BF stays at 4 (+8-12 % with 5).
-UNIT_DEFINES = {(0, 0, 0): ["-DSSSP_ARCS=5", "-DSSSP_SEG_HINT=0"], (1, 0, 0): ["-DSSSP_ARCS=5"]}
+# Phase B with dynamic per-CTA item assignment (SSSP_DYN_B) helps the rho and Delta* units
+# (rmat24 Delta* -3.1 %, rmat20 -3.4 %, rho -0.7 / -1 %) and costs BF 8-12 % (round 2 A/B).
+UNIT_DEFINES = {(0, 0, 0): ["-DSSSP_ARCS=5", "-DSSSP_SEG_HINT=0", "-DSSSP_DYN_B=1"],
+                (1, 0, 0): ["-DSSSP_ARCS=5", "-DSSSP_DYN_B=1"]}
 
 
 def units(unit_defines=None):
@@ -66,10 +69,13 @@ def up_to_date(out: str = OUT) -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=(), unit_defines=None) -> str:
+def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=(), unit_defines=None,
+          only_units=None) -> str:
     """Compile every translation unit (in parallel) and link the shared library.
     defines: tuning variants for every unit, e.g. SSSP_ARCS=4; unit_defines: {(pol, bidir,
-    fuse): ["-DNAME=VAL", ...]} added to one unit (both written to a separate `out`)."""
+    fuse): ["-DNAME=VAL", ...]} added to one unit (both written to a separate `out`).
+    only_units: names (e.g. {"inst_0_0_0", "pq"}) to compile; the other objects are taken
+    from the default build's object directory (A/B variants of one unit in seconds)."""
     if not force and out == OUT and not defines and not unit_defines and up_to_date():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
@@ -83,6 +89,11 @@ def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=(),
     def compile_one(u):
         name, src, extra = u
         obj = os.path.join(objdir, name + ".o")
+        if only_units is not None and name not in only_units:
+            import shutil
+
+            shutil.copyfile(os.path.join(os.path.dirname(objdir), "libsssp", name + ".o"), obj)
+            return name, obj, ["(copied from the default build)"], subprocess.CompletedProcess([], 0, "", "")
         cmd = [nvcc, *NVCC_FLAGS, *dflags, *extra, "-c", "-o", obj, src]
         res = subprocess.run(cmd, capture_output=True, text=True)
         return name, obj, cmd, res
@@ -110,7 +121,7 @@ def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=(),
 
 
 if __name__ == "__main__":
-    # python build.py [--force] [--out lib.so] [-DNAME=VAL ...] [--unit P,B,F:NAME=VAL ...]
+    # python build.py [--force] [--out lib.so] [-DNAME=VAL ...] [--unit P,B,F:NAME=VAL ...] [--only inst_0_0_0,...]
     args = sys.argv[1:]
     out = OUT
     if "--out" in args:
@@ -120,4 +131,8 @@ if __name__ == "__main__":
         if a == "--unit":
             key, d = args[i + 1].split(":")
             ud.setdefault(tuple(int(x) for x in key.split(",")), []).append("-D" + d)
-    build(force="--force" in args, out=out, defines=[a[2:] for a in args if a.startswith("-D")], unit_defines=ud)
+    only = None
+    if "--only" in args:
+        only = set(args[args.index("--only") + 1].split(","))
+    build(force="--force" in args, out=out, defines=[a[2:] for a in args if a.startswith("-D")], unit_defines=ud,
+          only_units=only)

@@ -323,11 +323,17 @@ struct WarpStage {
 #endif
     int32_t take[kTBuf];  // ids that pass the theta test, extracted 32 at a time
     int32_t q[kQBuf];     // ids appended to the next queue
+#if !defined(INST_BIDIR) || INST_BIDIR
     uint64_t mins[32];    // bidirectional relaxation: per-vertex pulled minimum
-    uint64_t pc[kPend];   // deferred WriteMins (kernels without fusion): candidate ...
+#endif
+#if !SSSP_FUSE_UNIT
+    uint64_t pc[kPend];   // deferred WriteMins (kernels without fusion or pull): candidate ...
     uint64_t pw[kPend];   // ... the word the filter read ...
     int32_t pv[kPend];    // ... and the target
+#endif
 };
+// (a unit's shared memory holds only the stage fields its kernels use: the rest of the 256 KB
+// of L1 / shared memory caches the filter reads of delta)
 struct FuseStage {        // FUSE kernels only (kept out of the others' shared memory, which is L1)
     uint64_t fd[kFBuf];   // fused vertices: key ...
     int32_t fid[kFBuf];   // ... id ...
@@ -596,6 +602,7 @@ __device__ __forceinline__ int write_min(uint64_t* dist, int32_t v, uint64_t c, 
 // for up to 32 of them), and stage the inserted ids.
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __device__ __forceinline__ void run_pending(const RunParams& p, Warp& W, int32_t cnt) {
+#if !SSSP_FUSE_UNIT
     const int lane = lane_id();
     __syncwarp();
     int out = kNone;
@@ -608,6 +615,7 @@ __device__ __forceinline__ void run_pending(const RunParams& p, Warp& W, int32_t
     __syncwarp();
     W.pn -= cnt;
     wq_push1(W, out == kAppend, v);
+#endif
 }
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __device__ __forceinline__ void drain_pending(const RunParams& p, Warp& W) {
@@ -634,6 +642,7 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
 #pragma unroll
     for (int t = 0; t < kArcs; t++) cur[t] = v[t] >= 0 ? dist_filter_ld(p.dist + v[t]) : 0ull;
     pull(v, cur, c);  // bidirectional relaxation may lower the candidates (SURVEY f-2)
+#if !SSSP_FUSE_UNIT
     if constexpr (!FUSE && !BIDIR) {
         // Deferred WriteMins: the improving candidates (a few per step in bulk rounds) are
         // staged and their CAS issued 32 at a time, so a step waits on its key gathers only,
@@ -655,7 +664,9 @@ __device__ __forceinline__ void relax_slots(const RunParams& p, const int32_t (&
         }
         PROF_ADD(W, 7, trs);
         return;
-    } else {
+    } else
+#endif
+    {
     // first CAS attempt of every slot issued back to back (one round trip, not kArcs),
     // then the rare retries
     uint64_t old[kArcs];
@@ -808,9 +819,11 @@ __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, i
 #pragma unroll
         for (int t = 0; t < kArcs; t++) cd[t] = dep + 1;
         const uint32_t fok = (FUSE && dep + 1 > p.fuse_depth) ? 0u : ~0u;
+#if !defined(INST_BIDIR) || INST_BIDIR
         if (BIDIR && __any_sync(kFull, uid >= 0))
             relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd, BidirPull{&p, W.st()->mins, o, wt, &d, uid});
         else
+#endif
             relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd);
         return;
     }
@@ -857,9 +870,11 @@ __device__ __forceinline__ void relax_vertices(const RunParams& p, uint64_t d, i
                 fok |= (cd[t] <= p.fuse_depth ? 1u : 0u) << t;
             }
         }
+#if !defined(INST_BIDIR) || INST_BIDIR
         if (BIDIR && bidir)
             relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd, BidirPull{&p, W.st()->mins, o, wt, &d, uid_step});
         else
+#endif
             relax_slots<POL, STATS, FUSE, BIDIR>(p, v, c, W, fok, cd);
     }
 }
@@ -1110,10 +1125,41 @@ __device__ __forceinline__ void phase_a(const RunParams& p, const Sharded<int32_
 }
 
 // --------------------------------------------------------------------- phase B
+#ifndef SSSP_DYN_B
+#define SSSP_DYN_B 0
+#endif
+// dyn_ctr != nullptr (SSSP_DYN_B, grid rounds): CTA c owns items c, c + grid, c + 2 grid, ...
+// and its warps take the next one from a shared-memory counter (no warp idles while its CTA
+// has items left); else warp gw strides over all items by nwarps.
 template <int POL, bool STATS, bool FUSE, bool BIDIR>
 __device__ __forceinline__ void phase_b(const RunParams& p, const Sharded<Desc>& CL, const int64_t* cpref, int32_t nl,
-                                        Warp& W, int64_t gw, int64_t nwarps) {
+                                        Warp& W, int64_t gw, int64_t nwarps, int32_t* dyn_ctr = nullptr) {
     const int lane = lane_id();
+    if (SSSP_DYN_B && dyn_ctr) {
+        const int64_t nc = cpref[kSeg];
+        int sh = 0;
+        auto take = [&]() {
+            int32_t k = 0;
+            if (lane == 0) k = atomicAdd(dyn_ctr, 1);
+            return (int64_t)__shfl_sync(kFull, k, 0) * gridDim.x + blockIdx.x;
+        };
+        auto chunk_at = [&](int64_t i) {
+            while (sh < kShards && cpref[sh + 1] <= i) sh++;  // a warp's items only increase
+            return ld_desc(CL.seg(sh) + (i - cpref[sh]));
+        };
+        int64_t item = take();
+        Desc nxt;
+        if (item < nc) nxt = chunk_at(item);
+        while (item < nc) {
+            const Desc e = nxt;
+            item = take();
+            if (item < nc) nxt = chunk_at(item);  // prefetch
+            relax_chunk<POL, STATS, FUSE, BIDIR>(p, e.d, e.beg, e.len, W);
+            if (FUSE && W.fn > kFBuf - 32 * kArcs) fuse_drain<POL, STATS, FUSE, BIDIR>(p, W);
+        }
+        fuse_drain<POL, STATS, FUSE, BIDIR>(p, W);
+        return;
+    }
     const int64_t nb = ((int64_t)nl + 31) / 32;
     const int64_t nc = cpref[kSeg];
     const int64_t total = nb + nc;
@@ -1620,7 +1666,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     __shared__ int64_t bc_dq;
     __shared__ int32_t bc_ext;           // extractions of the previous round (small-round entry test)
     __shared__ int32_t bc_nl, bc_cnt;
-    __shared__ int32_t tile_ctr[2];      // phase-A tile counters, by round parity
+    __shared__ int32_t tile_ctr[4];      // phase-A [0, 1] and phase-B [2, 3] item counters, by round parity
     __shared__ uint64_t red[kWarps];
     Ctrl* ctrl = p.ctrl;
     Warp W;
@@ -1631,7 +1677,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
 #if !SSSP_FUSE_UNIT
     if (lane_id() == 0) W.st()->ext = 0;
 #endif
-    if (threadIdx.x == 0) tile_ctr[0] = tile_ctr[1] = 0;
+    if (threadIdx.x == 0) tile_ctr[0] = tile_ctr[1] = tile_ctr[2] = tile_ctr[3] = 0;
     W.qdelta = 0;
 #if SSSP_PROF
     for (int i = 0; i < kProf; i++) W.prof[i] = 0;
@@ -1755,7 +1801,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         int64_t dense = 0;
         if (STATS && gtid == 0) t0 = tn = globaltimer();
         if (gtid == 0) reset_cnt(&ctrl->cnt[(r + 1) % 3]);
-        if (threadIdx.x == 0) tile_ctr[(r + 1) & 1] = 0;  // last used in round r-1's phase A
+        if (threadIdx.x == 0) tile_ctr[(r + 1) & 1] = tile_ctr[2 + ((r + 1) & 1)] = 0;  // last used in round r-1
         if (gtid < 2 * kSeg) {  // counters of slot (r+1)%3: written in round r+1, read in r+1 / r+2
             p.counters[((int64_t)(((r + 1) % 3) * 2) * kSeg + gtid) * kCntStride] = 0;
         }
@@ -1940,7 +1986,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         const bool phase_b_work = cpref[kSeg] + nl > 0;
         if (phase_b_work) {
             const uint64_t tb = STATS ? globaltimer() : 0;
-            phase_b<POL, STATS, FUSE, BIDIR>(p, CL, cpref, nl, W, warp_rank(), ((int64_t)gridDim.x * blockDim.x) >> 5);
+            phase_b<POL, STATS, FUSE, BIDIR>(p, CL, cpref, nl, W, warp_rank(), ((int64_t)gridDim.x * blockDim.x) >> 5,
+                                             nl == 0 ? &tile_ctr[2 + (r & 1)] : nullptr);
             if (STATS && lane_id() == 0) atomicAdd(&C->busy_b, (unsigned long long)(globaltimer() - tb));
         }
         drain_pending<POL, STATS, FUSE, BIDIR>(p, W);  // deferred WriteMins count in min_Q
@@ -2031,7 +2078,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         warm = ld_volatile_i32(&ctrl->sm_warm);
         split = kInf;  // small rounds list all of Q
         if (threadIdx.x == 0) {
-            tile_ctr[0] = tile_ctr[1] = 0;
+            tile_ctr[0] = tile_ctr[1] = tile_ctr[2] = tile_ctr[3] = 0;
             p.cta_delta[(r_new % 3) * kMaxCtas + blockIdx.x] = 0;
             p.cta_ext[(r_new % 3) * kMaxCtas + blockIdx.x] = 0;
         }

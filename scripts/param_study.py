@@ -121,6 +121,20 @@ def write_md(recs, path, traces=None):
     out = ["# Parameter study (SURVEY f-3), B200, one source per config (the workload source)", "",
            "Median device time of `sssp_run` over 3 runs (L2 flushed before each), default live rounds.", ""]
     cfgs, best, rows = fixed_rho(recs)
+    out += ["## Summary: best parameter per policy (ms, lower is better)", "",
+            "| config | BF | rho best (rho) | rho fixed" + (f" (2^{rows[0][2].bit_length() - 1})" if rows else "") +
+            " | Delta* best (Delta) | Delta-stepping best (Delta) |", "|---|---|---|---|---|---|"]
+    for c in dict.fromkeys(r["config"] for r in recs):
+        def bestof(pol):
+            rs = [r for r in recs if r["config"] == c and r["policy"] == pol]
+            return min(rs, key=lambda r: r["ms"]) if rs else None
+        cell = lambda r: "-" if r is None else (f"{r['ms']:.2f}" if r["policy"] == "bellman_ford" else  # noqa: E731
+                                                f"{r['ms']:.2f} (2^{r['param'].bit_length() - 1})")
+        fx = next((r for r in recs if rows and r["config"] == c and r["policy"] == "rho" and r["param"] == rows[0][2]), None)
+        out.append(f"| {c} | {cell(bestof('bellman_ford'))} | {cell(bestof('rho'))} | "
+                   f"{'-' if fx is None else format(fx['ms'], '.2f')} | {cell(bestof('delta'))} | "
+                   f"{cell(bestof('delta_stepping'))} |")
+    out.append("")
     if rows:
         geo, mx, p, loss = rows[0]
         out += [f"## One fixed GPU rho for all configs (PQ-rho-fix analogue, P:1575, P:1601)", "",
