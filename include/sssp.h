@@ -131,7 +131,8 @@ typedef struct {
     void *d_trace;          /* nullable device sssp_round[trace_cap]; filled when SSSP_RUN_STATS      */
     int64_t trace_cap;
     int32_t *d_ext_count;   /* nullable device int32[n]: extractions per vertex (Lemma num-ext) */
-    uint32_t fuse_depth;    /* fusion: hops a local search may go from its extracted seed (0 = default) */
+    uint32_t fuse_depth;    /* fusion: hops a local search may go from its extracted seed (0 = default:
+                               10 for rho-stepping, unbounded for Delta*-stepping) */
     uint32_t reserved;      /* must be 0 */
 } sssp_run_opts;
 

@@ -90,10 +90,18 @@ constexpr int kQBuf = 32 * kArcs > 256 ? 32 * kArcs : 256;  // staged queue ids 
 constexpr int kTBuf = 32 * kEnt + 32;        // staged extracted ids per warp
 constexpr int kFBuf = 32 * kArcs + 64;       // fused vertices waiting for their relax, per warp
 constexpr int kFuseBudget = SSSP_FUSE;       // fused vertices per warp per round (0 = off)
-#ifndef SSSP_FUSE_DEPTH
-#define SSSP_FUSE_DEPTH 1000000
+// Default bound on the hops a local search may go from its extracted seed (DESIGN.md §5
+// "fusion depth"; the paper bounds its local search by t = 4096 visited vertices).  A
+// round lasts as long as its slowest warp's local search: for rho-stepping, whose theta follows
+// the queue, 10 hops (with the per-warp budget of 64) cut grid4096 by 23 %, rgg4m by 14 % and
+// grid256 by 23 %.  Delta*-stepping's theta advances by Delta whatever the searches reached, so
+// a bound there can leave them behind theta (grid4096 Delta* 2^17 at 8 hops: 932 -> 2,706 rounds
+// of Bellman-Ford-like re-relaxation); its default stays unbounded (run.cu).
+#ifndef SSSP_FUSE_DEPTH_RHO
+#define SSSP_FUSE_DEPTH_RHO 10
 #endif
-constexpr int kFuseDepth = SSSP_FUSE_DEPTH;  // hops a local search may go from its extracted seed
+constexpr int kFuseDepthRho = SSSP_FUSE_DEPTH_RHO;
+constexpr int kFuseDepth = 1 << 30;  // unbounded
 constexpr int kFuseMaxDeg = 1024;            // a fused vertex of higher degree goes back to Q
 constexpr int kContigTiles = 16;             // queue < kContigTiles*32 ids per warp: contiguous shares
 constexpr int kSparseDeg = 20;               // fusion in rounds whose frontier averages < 20 arcs
@@ -1979,13 +1987,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         grid_sync();
         if (STATS && gtid == 0) t2 = globaltimer();
         // ---- phase B: heavy chunks (+ light list in snapshot mode)
+        if (threadIdx.x == 0) bc_nl = snap ? __ldcg(&C->nlight) : 0;  // (thread 0 is in warp 0: one barrier)
         load_prefix(CL, cpref);
-        if (threadIdx.x == 0) bc_nl = snap ? __ldcg(&C->nlight) : 0;
-        __syncthreads();
         const int32_t nl = bc_nl;
         const bool phase_b_work = cpref[kSeg] + nl > 0;
         if (phase_b_work) {
             const uint64_t tb = STATS ? globaltimer() : 0;
+            // (the snapshot-style rounds with a light list keep the static order: handling the
+            // light batches in the dynamic loop cost rmat24 rho 3 %, Delta* 6 %)
             phase_b<POL, STATS, FUSE, BIDIR>(p, CL, cpref, nl, W, warp_rank(), ((int64_t)gridDim.x * blockDim.x) >> 5,
                                              nl == 0 ? &tile_ctr[2 + (r & 1)] : nullptr);
             if (STATS && lane_id() == 0) atomicAdd(&C->busy_b, (unsigned long long)(globaltimer() - tb));

@@ -213,7 +213,8 @@ sssp_status launch_run(sssp_handle* h, int32_t source, sssp_policy policy, uint6
     p.trace_cap = o.trace_cap;
     p.ext_count = o.d_ext_count;
     p.fuse_budget = o.fuse_budget ? (int32_t)o.fuse_budget : kFuseBudget;
-    p.fuse_depth = o.fuse_depth ? (int32_t)std::min<uint32_t>(o.fuse_depth, 1u << 30) : kFuseDepth;
+    p.fuse_depth = o.fuse_depth ? (int32_t)std::min<uint32_t>(o.fuse_depth, 1u << 30)
+                                : (policy == SSSP_RHO ? kFuseDepthRho : kFuseDepth);
     const int mode = (fu ? 1 : 0) | ((o.flags & SSSP_RUN_BIDIR) ? 2 : 0);
     KernelFn k = kernel_for(policy, st, mode);
     const int grid = h->grid[policy][st][mode];
