@@ -32,11 +32,11 @@ sys.path.insert(0, ROOT)
 
 # best parameters of the parameter study (profiles/param_study_r1.md / param_study_r2.md)
 CASES = {
-    "grid256": [("delta", 1 << 17), ("rho", 1 << 10), ("bellman_ford", 0)],
-    "rmat20": [("rho", 1 << 16), ("delta", 1 << 15), ("bellman_ford", 0)],
+    "grid256": [("rho", 1 << 13), ("delta", 1 << 17), ("bellman_ford", 0)],
+    "rmat20": [("rho", 1 << 15), ("delta", 1 << 15), ("bellman_ford", 0)],
     "rgg4m": [("delta", 1 << 12), ("rho", 1 << 13), ("bellman_ford", 0)],
     "rmat24": [("rho", 1 << 18), ("delta", 1 << 17), ("bellman_ford", 0)],
-    "grid4096": [("delta", 1 << 17), ("rho", 1 << 14), ("bellman_ford", 0)],
+    "grid4096": [("rho", 1 << 14), ("delta", 1 << 17), ("bellman_ford", 0)],
 }
 LABEL = {"grid256": "C1 grid-256", "rmat20": "C2 R-MAT 20", "rgg4m": "C3 RGG-4M", "rmat24": "C4 R-MAT 24",
          "grid4096": "C5 grid-4096"}
