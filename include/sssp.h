@@ -125,7 +125,8 @@ sssp_status sssp_create(int32_t n, int64_t m, const int32_t *d_offsets, const in
 
 typedef struct {
     uint32_t flags;
-    uint32_t fuse_budget;   /* fusion: vertices a warp may extract on the spot per round (0 = default) */
+    uint32_t fuse_budget;   /* fusion: vertices a warp may extract on the spot per round (0 = default:
+                               96 for rho-stepping, 64 otherwise) */
     uint64_t seed;          /* rho sampling: counter-based generator seed (reading R6)      */
     int64_t max_rounds;     /* 0 = default (4n + 64); exceeded -> SSSP_ERR_ROUNDS                     */
     void *d_trace;          /* nullable device sssp_round[trace_cap]; filled when SSSP_RUN_STATS      */

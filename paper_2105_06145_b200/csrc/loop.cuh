@@ -90,6 +90,7 @@ constexpr int kQBuf = 32 * kArcs > 256 ? 32 * kArcs : 256;  // staged queue ids 
 constexpr int kTBuf = 32 * kEnt + 32;        // staged extracted ids per warp
 constexpr int kFBuf = 32 * kArcs + 64;       // fused vertices waiting for their relax, per warp
 constexpr int kFuseBudget = SSSP_FUSE;       // fused vertices per warp per round (0 = off)
+constexpr int kFuseBudgetRho = 96;           // the same for rho-stepping (bounded depth, run.cu)
 // Default bound on the hops a local search may go from its extracted seed (DESIGN.md §5
 // "fusion depth"; the paper bounds its local search by t = 4096 visited vertices).  A
 // round lasts as long as its slowest warp's local search: for rho-stepping, whose theta follows
@@ -1987,10 +1988,22 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
         grid_sync();
         if (STATS && gtid == 0) t2 = globaltimer();
         // ---- phase B: heavy chunks (+ light list in snapshot mode)
-        if (threadIdx.x == 0) bc_nl = snap ? __ldcg(&C->nlight) : 0;  // (thread 0 is in warp 0: one barrier)
-        load_prefix(CL, cpref);
-        const int32_t nl = bc_nl;
-        const bool phase_b_work = cpref[kSeg] + nl > 0;
+        bool phase_b_work;
+        int32_t nl = 0;
+        if (FUSE && !snap) {
+            // fusion rounds rarely emit chunks: every warp sums the 33 chunk counters itself
+            // (no CTA barrier), the prefix is built only if there is work (2.5 % on grid4096)
+            const int lane = lane_id();
+            int64_t c = CL.seg_count(lane);
+            if (lane == 0) c += CL.seg_count(kShards);
+            phase_b_work = warp_sum(c) > 0;  // (final after the grid barrier: the same in every warp)
+            if (phase_b_work) load_prefix(CL, cpref);
+        } else {
+            if (threadIdx.x == 0) bc_nl = snap ? __ldcg(&C->nlight) : 0;  // (thread 0 is in warp 0: one barrier)
+            load_prefix(CL, cpref);
+            nl = bc_nl;
+            phase_b_work = cpref[kSeg] + nl > 0;
+        }
         if (phase_b_work) {
             const uint64_t tb = STATS ? globaltimer() : 0;
             // (the snapshot-style rounds with a light list keep the static order: handling the

@@ -7,7 +7,8 @@
 #include <stdint.h>
 
 // mode 0: stream idx+w only; 1: + gather u64 dist[v]; 2: + gather u32 key[v];
-// 3: relax = gather + atomicMin(u64) when smaller (dist pre-filled so ~rate% succeed)
+// 3: relax = gather + atomicMin(u64) when smaller (dist pre-filled so ~rate% succeed);
+// 4: blind RED.MIN u64 on dist (no gather, no return); 5: blind RED.MIN u32 on key
 template <int MODE, int ARCS>
 __global__ void __launch_bounds__(512) k_relax(int64_t m, const int32_t* __restrict__ idx, const uint32_t* __restrict__ w,
                                                unsigned long long* dist, const uint32_t* key, unsigned long long* out) {
@@ -32,6 +33,14 @@ __global__ void __launch_bounds__(512) k_relax(int64_t m, const int32_t* __restr
         } else if (MODE == 2) {
 #pragma unroll
             for (int t = 0; t < ARCS; t++) acc += v[t] >= 0 ? __ldcg(key + v[t]) + ww[t] : 0;
+        } else if (MODE == 4) {  // blind WriteMin: RED.MIN (no return value, nothing waits on it)
+#pragma unroll
+            for (int t = 0; t < ARCS; t++)
+                if (v[t] >= 0) atomicMin(dist + v[t], (unsigned long long)ww[t] * 4);
+        } else if (MODE == 5) {  // blind RED.MIN on a 4n-byte (L2-resident) array
+#pragma unroll
+            for (int t = 0; t < ARCS; t++)
+                if (v[t] >= 0) atomicMin((unsigned*)key + v[t], ww[t] * 4u);
         } else {
             unsigned long long cur[ARCS];
 #pragma unroll
@@ -54,11 +63,11 @@ extern "C" float relax_bench(int mode, int arcs, int blocks, int64_t m, const in
     auto launch = [&]() {
 #define L(MO, AR) k_relax<MO, AR><<<blocks, 512>>>(m, idx, w, dist, key, out)
         if (arcs == 4) {
-            if (mode == 0) L(0, 4); else if (mode == 1) L(1, 4); else if (mode == 2) L(2, 4); else L(3, 4);
+            if (mode == 0) L(0, 4); else if (mode == 1) L(1, 4); else if (mode == 2) L(2, 4); else if (mode == 3) L(3, 4); else if (mode == 4) L(4, 4); else L(5, 4);
         } else if (arcs == 8) {
-            if (mode == 0) L(0, 8); else if (mode == 1) L(1, 8); else if (mode == 2) L(2, 8); else L(3, 8);
+            if (mode == 0) L(0, 8); else if (mode == 1) L(1, 8); else if (mode == 2) L(2, 8); else if (mode == 3) L(3, 8); else if (mode == 4) L(4, 8); else L(5, 8);
         } else {
-            if (mode == 0) L(0, 16); else if (mode == 1) L(1, 16); else if (mode == 2) L(2, 16); else L(3, 16);
+            if (mode == 0) L(0, 16); else if (mode == 1) L(1, 16); else if (mode == 2) L(2, 16); else if (mode == 3) L(3, 16); else if (mode == 4) L(4, 16); else L(5, 16);
         }
 #undef L
     };

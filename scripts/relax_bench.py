@@ -22,8 +22,10 @@ dist = torch.randint(0, 1 << 40, (g.n,), dtype=torch.int64, device="cuda")
 key = torch.randint(0, 1 << 30, (g.n,), dtype=torch.int32, device="cuda")
 out = torch.zeros(4, dtype=torch.int64, device="cuda")
 m = g.m
-names = {0: "stream idx+w", 1: "+gather u64", 2: "+gather u32", 3: "+gather u64+atomicMin"}
-for mode in (0, 1, 2, 3):
+names = {0: "stream idx+w", 1: "+gather u64", 2: "+gather u32", 3: "+gather u64+atomicMin", 4: "+blind RED.MIN u64",
+         5: "+blind RED.MIN u32"}
+modes = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 1, 2, 3, 4, 5]
+for mode in modes:
     for arcs in (4, 8, 16):
         for bpsm in (2, 4):
             blocks = 148 * bpsm
