@@ -35,8 +35,11 @@ POLICIES = 5  # SSSP_RHO .. SSSP_DELTA_STEPPING (include/sssp.h)
 # The Delta* unit likewise (rmat24 -1.6 %, rmat20 -2.4 %); BF stays at 4 (+8-12 % with 5).
 # Phase B with dynamic per-CTA item assignment (SSSP_DYN_B) helps the rho and Delta* units
 # (rmat24 Delta* -3.1 %, rmat20 -3.4 %, rho -0.7 / -1 %) and costs BF 8-12 % (round 2 A/B).
+# The static order's next descriptor by cp.async (SSSP_NEXT_SMEM) lost 4.6 % on BF, which keeps
+# it in registers.
 UNIT_DEFINES = {(0, 0, 0): ["-DSSSP_ARCS=5", "-DSSSP_SEG_HINT=0", "-DSSSP_DYN_B=1"],
-                (1, 0, 0): ["-DSSSP_ARCS=5", "-DSSSP_DYN_B=1"]}
+                (1, 0, 0): ["-DSSSP_ARCS=5", "-DSSSP_DYN_B=1"],
+                (2, 0, 0): ["-DSSSP_NEXT_SMEM=0"]}
 
 
 def units(unit_defines=None):

@@ -36,6 +36,12 @@ __device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p) {
 __device__ __forceinline__ void ld_row(const int32_t* off, int32_t i, int32_t& beg, int32_t& end) {
     asm volatile("ld.global.nc.s32 %0, [%2];\n\tld.global.nc.s32 %1, [%2+4];" : "=r"(beg), "=r"(end) : "l"(off + i));
 }
+// 16-byte global -> shared copy through L2 (no register holds the data in between)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ uint64_t atom_or_u64(uint64_t* p, uint64_t x) {
     uint64_t old;
     asm volatile("atom.global.or.b64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(x) : "memory");
