@@ -28,8 +28,8 @@ POLICIES = 5  # SSSP_RHO .. SSSP_DELTA_STEPPING (include/sssp.h)
 # fusion kernels spill with it).  Before deferred WriteMins, 6 arcs: rmat24 rho = 2^18
 # -2.6 %, 2^21 -6 % against 4.
 # The segment hint in phase B (forward scan instead of a binary search per descriptor)
-# helps BF / Delta* by ~2 % and costs the 6-arc rho unit ~2 % (register allocation), so
-# that unit keeps the binary search.
+# helps BF / Delta* by ~2 %; the rho unit kept the binary search while the next descriptor
+# lived in registers (round 1), and gains 0.3-1.2 % from the hint since it moved to cp.async.
 # With deferred WriteMins the rho unit does best at 5 arcs per lane (A/B against 6:
 # rmat24 rho = 2^18 -2.9 %, 2^17 -3.1 %, rmat20 -4 %; 7 arcs: +2 %).
 # The Delta* unit likewise (rmat24 -1.6 %, rmat20 -2.4 %); BF stays at 4 (+8-12 % with 5).
@@ -37,7 +37,7 @@ POLICIES = 5  # SSSP_RHO .. SSSP_DELTA_STEPPING (include/sssp.h)
 # (rmat24 Delta* -3.1 %, rmat20 -3.4 %, rho -0.7 / -1 %) and costs BF 8-12 % (round 2 A/B).
 # The static order's next descriptor by cp.async (SSSP_NEXT_SMEM) lost 4.6 % on BF, which keeps
 # it in registers.
-UNIT_DEFINES = {(0, 0, 0): ["-DSSSP_ARCS=5", "-DSSSP_SEG_HINT=0", "-DSSSP_DYN_B=1"],
+UNIT_DEFINES = {(0, 0, 0): ["-DSSSP_ARCS=5", "-DSSSP_DYN_B=1"],
                 (1, 0, 0): ["-DSSSP_ARCS=5", "-DSSSP_DYN_B=1"],
                 (2, 0, 0): ["-DSSSP_NEXT_SMEM=0"]}
 
