@@ -85,7 +85,10 @@ constexpr int kWarps = kBlock / 32;
 #ifndef SSSP_FUSE
 #define SSSP_FUSE 64
 #endif
-constexpr int kEnt = 2;                      // queue entries per lane per Extract step (large queues)
+#ifndef SSSP_ENT
+#define SSSP_ENT 2
+#endif
+constexpr int kEnt = SSSP_ENT;               // queue entries per lane per Extract step (large queues)
 constexpr int kQBuf = 32 * kArcs > 256 ? 32 * kArcs : 256;  // staged queue ids per warp (>= 32 * kArcs)
 constexpr int kTBuf = 32 * kEnt + 32;        // staged extracted ids per warp
 constexpr int kFBuf = 32 * kArcs + 64;       // fused vertices waiting for their relax, per warp
@@ -1729,6 +1732,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     __shared__ int32_t bc_nl, bc_cnt;
     __shared__ int32_t tile_ctr[4];      // phase-A [0, 1] and phase-B [2, 3] item counters, by round parity
     __shared__ uint64_t red[kWarps];
+#ifndef SSSP_BAL
+#define SSSP_BAL 0
+#endif
+#if SSSP_BAL
+    __shared__ unsigned long long bal[2];
+    if (threadIdx.x == 0) bal[0] = bal[1] = 0;
+#endif
     Ctrl* ctrl = p.ctrl;
     Warp W;
     W.init();
@@ -2020,7 +2030,22 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
 #if SSSP_PROF
             for (int i = 0; i < kProf; i++) atomicAdd(&C->prof[i], (unsigned long long)W.prof[i]);
 #endif
+#if SSSP_BAL  // balance probe: per-CTA sum and max of the warps' phase-A busy time
+            atomicAdd(&bal[0], ba);
+            atomicMax(&bal[1], ba);
+#endif
         }
+#if SSSP_BAL
+        if (STATS) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                atomicMax(&C->prof[0], bal[0] / kWarps);  // max over CTAs of the CTA-mean busy
+                atomicAdd(&C->prof[1], bal[0] / kWarps);  // sum over CTAs of the CTA-mean busy
+                atomicAdd(&C->prof[2], bal[1]);           // sum over CTAs of the CTA-max busy
+                bal[0] = bal[1] = 0;
+            }
+        }
+#endif
 #if SSSP_PROF
         for (int i = 0; i < kProf; i++) W.prof[i] = 0;
 #endif

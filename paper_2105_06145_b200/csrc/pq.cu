@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kPQBlock) pq_hist_kernel(const uint64_t* __res
     const int wid = threadIdx.x >> 5;
     for (int b = threadIdx.x; b < kW * 256; b += blockDim.x) (&h[0][0])[b] = 0;
     __syncthreads();
-    constexpr int U = 8;
+    constexpr int U = 16;
     const int64_t step = (int64_t)gridDim.x * blockDim.x * U;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x; base < q; base += step) {
         uint64_t x[U];
@@ -531,8 +531,10 @@ sssp_status sssp_pq_select(sssp_pq* q, uint64_t rho, uint64_t seed, uint32_t mod
     if (mode == SSSP_SELECT_EXACT) {
         pq_minmax_kernel<<<q->grid, kPQBlock, 0, q->stream>>>(q->q[q->cur], q->keys, rho, q->kbuf, q->samples, q->ctrl,
                                                               q->sel);
+        // (a quarter of the grid: each CTA adds 256 counters and takes the last-CTA ticket with
+        // same-address atomics, which dominated a pass at 1,184 CTAs: ~30 us for a 58 MB stream)
         for (int pass = 0; pass < 8; pass++)  // 64-bit keys: at most 8 digits
-            pq_hist_kernel<<<q->grid, kPQBlock, 0, q->stream>>>(q->kbuf, q->ctrl, q->sel);
+            pq_hist_kernel<<<q->grid / 4, kPQBlock, 0, q->stream>>>(q->kbuf, q->ctrl, q->sel);
     } else {
         pq_select_kernel<<<1, kSelBlock, 0, q->stream>>>(q->q[q->cur], q->keys, rho, seed, mode, q->samples, q->ctrl);
     }
