@@ -48,6 +48,12 @@
 
 namespace sssp {
 
+// (a kernel unit is compiled for one fusion flag, INST_FUSE; run.cu sees neither)
+#if defined(INST_FUSE) && INST_FUSE
+#define SSSP_FUSE_UNIT 1
+#else
+#define SSSP_FUSE_UNIT 0
+#endif
 #ifndef SSSP_MIN_BLOCKS
 #define SSSP_MIN_BLOCKS 1
 #endif
@@ -67,7 +73,21 @@ constexpr int kMinBlocks = SSSP_MIN_BLOCKS;  // CTAs per SM the register budget 
 constexpr int kArcs = SSSP_ARCS;             // arcs per lane in flight
 constexpr int kChunk = 32 * kArcs;           // arcs per heavy-chunk descriptor
 constexpr int kLight = SSSP_LIGHT;           // out-degree <= kLight: relaxed by the extracting warp
-constexpr int kSmemSamples = 2048;           // theta samples held in shared memory (else CTA-0 fallback)
+// Shared-memory budget: L1 is what the carveout leaves of the SM's 256 KB, and the carveout
+// comes in steps (.., 64, 100, 132, 164, .. KB).  The relax's in-flight loads live in L1 lines,
+// so every unit is sized to fall just under a step (DESIGN.md §5 "shared memory per unit"):
+// units without fusion 98.8 KB -> the 100 KB step (from 123 KB / 132: rmat24 rho -2.3 %, Delta*
+// and BF -3.9 %, rmat20 -2 to -3 %), fusion units 134.9 KB -> 132 (from 164: road graphs -0.5
+// to -0.9 %).  What shrank: theta samples held in shared memory (more fall back to CTA 0 and a
+// barrier), the per-warp append stage, and the small-round queue.
+#ifndef SSSP_SMEM_SAMPLES
+#if SSSP_FUSE_UNIT
+#define SSSP_SMEM_SAMPLES 480
+#else
+#define SSSP_SMEM_SAMPLES 512
+#endif
+#endif
+constexpr int kSmemSamples = SSSP_SMEM_SAMPLES;  // theta samples held in shared memory (else CTA-0 fallback)
 #ifndef SSSP_RANK_SELECT
 #define SSSP_RANK_SELECT 256
 #endif
@@ -89,7 +109,14 @@ constexpr int kWarps = kBlock / 32;
 #define SSSP_ENT 2
 #endif
 constexpr int kEnt = SSSP_ENT;               // queue entries per lane per Extract step (large queues)
-constexpr int kQBuf = 32 * kArcs > 256 ? 32 * kArcs : 256;  // staged queue ids per warp (>= 32 * kArcs)
+#ifndef SSSP_QBUF
+#if SSSP_FUSE_UNIT
+#define SSSP_QBUF 128
+#else
+#define SSSP_QBUF 224
+#endif
+#endif
+constexpr int kQBuf = 32 * kArcs > SSSP_QBUF ? 32 * kArcs : SSSP_QBUF;  // staged queue ids per warp (>= 32 * kArcs)
 constexpr int kTBuf = 32 * kEnt + 32;        // staged extracted ids per warp
 constexpr int kFBuf = 32 * kArcs + 64;       // fused vertices waiting for their relax, per warp
 constexpr int kFuseBudget = SSSP_FUSE;       // fused vertices per warp per round (0 = off)
@@ -322,12 +349,6 @@ __device__ __forceinline__ int seg_of(const int64_t* pref, int64_t i) {
 
 // --------------------------------------------------------------------- per-warp staging
 constexpr int kPend = 64;  // deferred WriteMins: pending WriteMins per warp (drained at 32)
-// (a kernel unit is compiled for one fusion flag, INST_FUSE; run.cu sees neither)
-#if defined(INST_FUSE) && INST_FUSE
-#define SSSP_FUSE_UNIT 1
-#else
-#define SSSP_FUSE_UNIT 0
-#endif
 struct WarpStage {
     Desc nd[2];           // phase B (dynamic items): the next chunk descriptor, copied in by cp.async
 #if !SSSP_FUSE_UNIT
@@ -364,7 +385,10 @@ struct FuseStage {        // FUSE kernels only (kept out of the others' shared m
 // Kernels with fusion do not run small rounds: there a small |Q| hides the fused work, and the
 // path cost them 3-6 % (A/B on grid256 / grid4096 / rgg4m); the others gain from it.
 __host__ __device__ constexpr bool small_on(bool fuse) { return SSSP_SMALL && !fuse; }
-constexpr int kSmallQ = 2048;
+#ifndef SSSP_SMALL_Q
+#define SSSP_SMALL_Q 1024
+#endif
+constexpr int kSmallQ = SSSP_SMALL_Q;
 constexpr int kSmallArcs = 32768;
 #ifndef SSSP_SMALL_F
 #define SSSP_SMALL_F 256

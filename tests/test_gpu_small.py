@@ -1,4 +1,4 @@
-"""GPU parity of the small-frontier rounds: while |Q| <= 2048 and a round's
+"""GPU parity of the small-frontier rounds: while |Q| <= 1024 and a round's
 frontier has <= 32768 arcs, CTA 0 runs the rounds alone and hands them back to the grid.
 
 Every hand-over direction is exercised: entry at round 1, exit because |Q| outgrew the
@@ -77,7 +77,7 @@ def test_small_rounds_parity(cuda_device, name):
 
 def test_small_rounds_handoffs(cuda_device):
     """hub_chain under Bellman-Ford: small from round 1, the hub's round handed to the grid
-    (too many arcs), the leaves' round on the grid (|Q| > 2048), small again on the tail."""
+    (too many arcs), the leaves' round on the grid (|Q| > 1024), small again on the tail."""
     import paper_2105_06145_b200 as P
 
     g = hub_chain()
