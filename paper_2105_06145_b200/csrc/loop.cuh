@@ -1395,7 +1395,7 @@ __device__ __forceinline__ void far_to_near(const RunParams& p, const Sharded<in
     const Sharded<int32_t> saved = W.swap_qnext(L);
     const int64_t gw = warp_rank();
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    constexpr int kV = 8;
+    constexpr int kV = 8;  // keys in flight per lane per step (12 / 16: +0 to +1.7 %, registers)
     for (int64_t base = gw * (32 * kV); base < p.n; base += nwarps * (32 * kV)) {
         uint64_t x[kV];
 #pragma unroll
@@ -2234,23 +2234,43 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_round_loop(RunParams 
     if (gtid == 0) ctrl->rounds = r - 1;
     // S6 output: strip the flag bit (every reached vertex was extracted; INF stays INF)
     if (p.nofo) {  // compacted ids: out[v] = delta[nofo[v]] for every caller id v
-        // 4 consecutive ids per thread per step (one 16-byte map load, 4 key loads in
-        // flight); nofo is a 256-byte-aligned workspace array
-        const int64_t n4 = p.n_out & ~3ll;
-        for (int64_t v = gtid * 4; v < n4; v += gsize * 4) {
-            const int4 u4 = __ldcg((const int4*)(p.nofo + v));
-            const int32_t u[4] = {u4.x, u4.y, u4.z, u4.w};
-            uint64_t x[4];
+        // A warp maps 512 consecutive ids per step: 4 coalesced 16-byte map loads per lane, then
+        // 16 key loads in flight, then the stores (16-byte ones if the caller's array allows).
+        // The pass is a chain of two dependent loads per step, so its length is steps per warp:
+        // 7 on rmat24 (it was 28 with 4 ids per thread per step).  nofo is a 256-byte-aligned
+        // workspace array.
+        const auto strip = [](uint64_t x) { return (x != kInf && (x & kTop)) ? (x & kVal) : x; };
+        const int64_t nblk = p.n_out / 512;
+        const bool al16 = ((uintptr_t)p.out & 15) == 0;
+        for (int64_t blk = gtid >> 5; blk < nblk; blk += gsize >> 5) {
+            const int64_t v0 = blk * 512 + lane_id() * 4;
+            int4 u4[4];
 #pragma unroll
-            for (int k = 0; k < 4; k++)
-                x[k] = (u[k] < p.n || u[k] == src) ? __ldcg((const unsigned long long*)(p.dist + u[k])) : kInf;
+            for (int k = 0; k < 4; k++) u4[k] = __ldcg((const int4*)(p.nofo + v0 + k * 128));
+            uint64_t x[16];
 #pragma unroll
-            for (int k = 0; k < 4; k++) p.out[v + k] = (x[k] != kInf && (x[k] & kTop)) ? (x[k] & kVal) : x[k];
+            for (int k = 0; k < 4; k++) {
+                const int32_t u[4] = {u4[k].x, u4[k].y, u4[k].z, u4[k].w};
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    x[k * 4 + j] = (u[j] < p.n || u[j] == src) ? __ldcg((const unsigned long long*)(p.dist + u[j])) : kInf;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                uint64_t* o = p.out + v0 + k * 128;
+                if (al16) {
+                    *(ulonglong2*)o = make_ulonglong2(strip(x[k * 4]), strip(x[k * 4 + 1]));
+                    *(ulonglong2*)(o + 2) = make_ulonglong2(strip(x[k * 4 + 2]), strip(x[k * 4 + 3]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; j++) o[j] = strip(x[k * 4 + j]);
+                }
+            }
         }
-        for (int64_t v = n4 + gtid; v < p.n_out; v += gsize) {
+        for (int64_t v = nblk * 512 + gtid; v < p.n_out; v += gsize) {
             const int32_t u = p.nofo[v];
             const uint64_t x = (u < p.n || u == src) ? __ldcg((const unsigned long long*)(p.dist + u)) : kInf;
-            p.out[v] = (x != kInf && (x & kTop)) ? (x & kVal) : x;
+            p.out[v] = strip(x);
         }
     } else {
         for (int64_t i = gtid; i < p.n; i += gsize) {
