@@ -371,6 +371,33 @@ def test_unaligned_output_buffer(cuda_device):
             _assert_same(P.dist_to_u64(out), want, f"offset {off}/rho {par}/stats")
 
 
+def test_compacted_output_ragged_tail(cuda_device):
+    """The compacted runs' output pass maps 512 caller ids per warp step and finishes the ragged
+    tail (n mod 512) one id per thread: a dense graph over the first 2,600 of n = 3,001 ids (the
+    rest isolated, so the compaction applies and the tail holds isolated vertices), with a
+    16- and an 8-byte aligned output array, against the oracle."""
+    import torch
+
+    P = _P()
+    rs = np.random.default_rng(77)
+    n, k = 3001, 2600
+    src = rs.integers(0, k, 80000)
+    dst = rs.integers(0, k, 80000)
+    w = rs.integers(1, 1 << 12, 80000).astype(np.uint32)
+    g = gen.from_arcs(n, src, dst, w, symmetrise=True, source=5)
+    deg = np.diff(g.offsets.astype(np.int64))
+    assert g.m >= 20 * g.n and int((deg == 0).sum()) >= g.n // 16 and g.n % 512 != 0
+    want = oracle.dijkstra(g)
+    h = P.SSSP.from_graph(g)
+    base = torch.empty(g.n + 2, dtype=torch.int64, device="cuda")
+    for off in (0, 1):
+        out = base[off:off + g.n]
+        for pol, par in (("rho", 64), ("bellman_ford", 0), ("delta", 256)):
+            out.fill_(-7)
+            h.run(g.source, pol, par, out=out)
+            _assert_same(P.dist_to_u64(out), want, f"ragged tail offset {off} {pol}")
+
+
 def test_isolated_vertex_compaction(cuda_device):
     """Power-law graphs with many isolated vertices are renumbered inside the handle (the
     non-isolated ones become 0..nz-1); sources map in and distances / extraction counts map
