@@ -35,7 +35,7 @@ CASES = {
     "grid256": [("rho", 1 << 13), ("delta", 1 << 17), ("bellman_ford", 0)],
     "rmat20": [("rho", 1 << 15), ("delta", 1 << 15), ("bellman_ford", 0)],
     "rgg4m": [("delta", 1 << 12), ("rho", 1 << 14), ("bellman_ford", 0)],
-    "rmat24": [("rho", 1 << 18), ("delta", 1 << 17), ("bellman_ford", 0)],
+    "rmat24": [("rho", 360000), ("rho", 1 << 18), ("delta", 1 << 17), ("bellman_ford", 0)],
     "grid4096": [("rho", 1 << 14), ("delta", 1 << 17), ("bellman_ford", 0)],
 }
 LABEL = {"grid256": "C1 grid-256", "rmat20": "C2 R-MAT 20", "rgg4m": "C3 RGG-4M", "rmat24": "C4 R-MAT 24",
@@ -175,7 +175,8 @@ def write_md(recs, path, ncu=None):
            "δ == oracle | oracle s (1 thread) | oracle MTEPS |",
            "|" + "---|" * 18]
     for r in recs:
-        par = "-" if r["policy"] == "bellman_ford" else f"2^{r['param'].bit_length() - 1}"
+        par = "-" if r["policy"] == "bellman_ford" else (
+            f"2^{r['param'].bit_length() - 1}" if r["param"] & (r["param"] - 1) == 0 else f"{r['param']:,}")
         nc = lambda k, f: (f.format(r[k]) if k in r else "-")  # noqa: E731
         out.append(f"| {LABEL[r['config']]} | {r['n']:,} | {r['m']:,} | {r['policy']} {par} | {r['rounds']:.0f} | "
                    f"{r['ms']:.3f} | {r['gteps']:.2f} | {r['b_touched'] / 1e9:.3f} | {r['touched_gbs']:.0f} | "

@@ -20,7 +20,8 @@ CASES = {
                ("delta_stepping", 1 << 13), ("dijkstra", 0)],
     "rgg4m": [("rho", 1 << 12), ("rho", 1 << 15), ("delta", 1 << 8), ("bellman_ford", 0),
               ("delta_stepping", 1 << 10)],
-    "rmat24": [("rho", 1 << 15), ("rho", 1 << 18), ("rho", 1 << 21), ("delta", 1 << 15), ("bellman_ford", 0)],
+    "rmat24": [("rho", 360000), ("rho", 1 << 15), ("rho", 1 << 18), ("rho", 1 << 21), ("delta", 1 << 15),
+               ("bellman_ford", 0)],
     "grid4096": [("rho", 1 << 12), ("delta", 1 << 13), ("bellman_ford", 0)],
 }
 
