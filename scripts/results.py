@@ -33,7 +33,7 @@ sys.path.insert(0, ROOT)
 # best parameters of the parameter study (profiles/param_study_r1.md / param_study_r2.md)
 CASES = {
     "grid256": [("rho", 1 << 13), ("delta", 1 << 17), ("bellman_ford", 0)],
-    "rmat20": [("rho", 1 << 15), ("delta", 1 << 15), ("bellman_ford", 0)],
+    "rmat20": [("rho", 56000), ("rho", 1 << 15), ("delta", 1 << 15), ("bellman_ford", 0)],
     "rgg4m": [("delta", 1 << 12), ("rho", 1 << 14), ("bellman_ford", 0)],
     "rmat24": [("rho", 360000), ("rho", 1 << 18), ("delta", 1 << 17), ("bellman_ford", 0)],
     "grid4096": [("rho", 1 << 14), ("delta", 1 << 17), ("bellman_ford", 0)],
