@@ -27,10 +27,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # rho = 360,000: the tuned rho of rmat24 (PQ-rho-best).  The power-of-two study puts the best rho at
-# 2^18; a finer sweep between 2^18 and the cliff at ~450,000, where the warm-up rounds extract the
-# hubs too early and every arc is relaxed 1.56 times, keeps gaining (profiles/param_study_r2_fine.md:
-# 2^18 3.75 ms, 360,000 3.63 ms, 400,000 3.60 ms over 20 sampling seeds each).  360,000 leaves a 20 %
-# margin below the cliff.
+# 2^18; a finer sweep between 2^18 and the cliff keeps gaining (profiles/param_study_r2_fine.md:
+# 2^18 3.75 ms, 360,000 3.63 ms, 400,000 3.60 ms over 20 sampling seeds each).  The cliff is the
+# source's degree, 406,678 = |Q_2|: from there on |Q_2| <= rho makes theta_2 = +inf, the whole
+# first frontier is extracted with tentative keys and every arc is relaxed 1.56 times (4.77 ms at
+# 450,000, as at 2^19).  360,000 leaves an 11 % margin below it.
 DEFAULT_PARAM = {"rho": 360000, "delta": 1 << 15, "bellman_ford": 0, "dijkstra": 0}
 PAPER_RHO_FIX = 1 << 21  # PQ-rho-fix on scale-free graphs
 CONFIG_DESC = {
